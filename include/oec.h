@@ -1,0 +1,234 @@
+/*
+ * oec.h -- C ABI of liboec, the B200-native hot path of the Open Earth Compiler paper
+ * (arXiv 2005.13014, "PAPER.md" below): fused fp64 stencil programs on 3D fields with halos.
+ *
+ * A STENCIL PROGRAM "loads the data from the input arrays, implements the stencil operators
+ * inline, and stores the results to the output arrays" (§4.4).  Every entry
+ * point below applies one such program, fused into a single pass over HBM (stencil inlining,
+ * §5.1; "we do not need to store and load any temporary buffer, and all inputs of the
+ * stencil program are only loaded once", §7.3), to a caller-given domain.
+ *
+ * ---------------------------------------------------------------------------------------------
+ * Conventions (apply to every call)
+ * ---------------------------------------------------------------------------------------------
+ * Coordinates.  Absolute integer (i, j, k) coordinates whose origin is the lower bound of the
+ *   computation domain the fields were made for ("The origin denotes the lower bound of the
+ *   computation domain and has all coordinates set to zero", §4.2).  Ranges are
+ *   [lb, ub): inclusive lower, exclusive upper bound.  i is the fastest dimension.
+ * Fields.  An oec_field describes (does not own, unless `owned`) a strided fp64 array over its
+ *   ALLOCATED range [lb, ub): element (i,j,k) lives at
+ *     data + (i-lb[0])*stride[0] + (j-lb[1])*stride[1] + (k-lb[2])*stride[2]   (elements).
+ *   stride[0] must be 1.  A k-invariant ("2D metric") field has lb[2] = 0, ub[2] = 1 and
+ *   stride[2] = 0 and is broadcast along k.
+ * Domain.  dom_lb/dom_ub select the points computed; outputs are written ONLY there (the
+ *   stencil.store range).  Output halos and padding are never written.
+ * Extents.  Each input must cover the domain grown by that program's access extent (shape
+ *   inference, §5.2: "verify the input array is large enough"); see
+ *   oec_program_input().  Otherwise OEC_ERR_SHAPE.  There is no boundary condition: input
+ *   halos are caller data (operators compute "all elements ... except for some constant-width
+ *   boundary").
+ * Aliasing.  "All stencil program parameters have to be alias-free and are either loaded from
+ *   or stored to as a unit".  An output whose bytes overlap any input or another
+ *   output -> OEC_ERR_ALIAS.
+ * Memory / ownership.  device >= 0: `data` is device memory of that CUDA ordinal; the call
+ *   validates synchronously and ENQUEUES the kernel(s) on `stream` (a cudaStream_t passed as
+ *   void*, NULL = legacy default stream); it never synchronises.  device == OEC_DEVICE_HOST:
+ *   `data` is host memory (pinned or pageable); the library stages it through a cached device
+ *   workspace on the current device: H2D copies of the inputs, the kernel, D2H copies of the
+ *   outputs' domain, then it synchronises `stream` before returning (the end-to-end path).
+ *   All fields of one call must be on the same side.
+ * Numerics.  IEEE fp64, round-to-nearest-even, no contraction into FMA, expression order of the
+ *   program definitions in DESIGN.md: results are bit-identical to the CPU oracle.
+ * Errors.  Every call returns an oec_status; OEC_OK = 0.  No exception crosses the ABI.  The
+ *   message of the last failing call on this thread is oec_last_error().  Launch failures are
+ *   OEC_ERR_CUDA; asynchronous device faults surface at the caller's next synchronisation.
+ * Threading.  Calls are thread-safe; state is per-thread (last error) or per object (decomp).
+ */
+#ifndef OEC_H
+#define OEC_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define OEC_ABI_VERSION 1
+#define OEC_DEVICE_HOST (-1)
+
+typedef enum {
+    OEC_OK = 0,
+    OEC_ERR_ARG = 1,         /* NULL pointer, bad enum, unknown program, wrong arg count     */
+    OEC_ERR_SHAPE = 2,       /* allocation does not cover domain + extent, K < 2 (vadv), ... */
+    OEC_ERR_ALIAS = 3,       /* an output overlaps an input or another output         */
+    OEC_ERR_DTYPE = 4,       /* dtype other than OEC_F64, or mixed devices                   */
+    OEC_ERR_CUDA = 5,        /* CUDA runtime error (launch, allocation, copy)                */
+    OEC_ERR_NCCL = 6,        /* NCCL error or NCCL not loadable                               */
+    OEC_ERR_UNSUPPORTED = 7, /* valid request this build does not implement                  */
+    OEC_ERR_LAYOUT = 8       /* stride[0] != 1, misaligned data, offsets overflow int32      */
+} oec_status;
+
+typedef enum { OEC_F64 = 0 } oec_dtype;
+
+/* Kernel variants of oec_apply_program / oec_hdiff_variant.                                   */
+typedef enum {
+    OEC_VARIANT_AUTO = 0,  /* fastest B200 kernel (default)                                     */
+    OEC_VARIANT_NAIVE = 2  /* the paper's execution model: one thread per point, every producer
+                              inlined and recomputed, registers only, no shared memory and no
+                              synchronisation -- kept for comparison            */
+} oec_variant;
+
+typedef struct oec_field {
+    void *data;        /* element (lb[0], lb[1], lb[2]); device or host memory (see `device`) */
+    int64_t lb[3];     /* allocated range, absolute coordinates (origin = domain lower bound)  */
+    int64_t ub[3];
+    int64_t stride[3]; /* elements; stride[0] == 1; stride[2] == 0 for k-invariant fields      */
+    int32_t dtype;     /* oec_dtype                                                            */
+    int32_t device;    /* CUDA ordinal, or OEC_DEVICE_HOST                                     */
+    int32_t owned;     /* 1: allocated by oec_field_create, freed by oec_field_destroy         */
+    int32_t reserved;
+} oec_field;
+
+/* ABI version (OEC_ABI_VERSION) and a static build-info string. */
+int32_t oec_abi_version(void);
+const char *oec_build_info(void);
+
+/* Message for the last non-OK status returned on this thread ("" if none). */
+const char *oec_last_error(void);
+
+/* Allocate a device field covering [-halo_lo, domain + halo_hi) per dim (a0 of SURVEY §8(a)).
+ *   domain[3]    interior extent (Ni, Nj, Nk), each >= 1 (k: >= 1; use Nk = 1, halo 0 and
+ *                k_invariant = 1 for 2D metric fields)
+ *   halo_lo/hi   halo widths per dim, 0 <= h <= 16 in i (the left pad), any >= 0 in j, k
+ *   order        NULL = default {0, 2, 1}: i fastest, then k, then j (a j-slab halo is one
+ *                contiguous block); or a permutation of {0,1,2}
+ *                listing dims fastest -> slowest (order[0] must be 0)
+ *   k_invariant  1: 2D field broadcast along k (requires domain[2] == 1, halo k == 0)
+ * Layout: i rows start 16 elements left of i = 0 so that i = 0 is 128-byte aligned; the row
+ * pitch is a multiple of 16 elements (128 B).  Memory is cudaMalloc'ed on `device` and zeroed.
+ * out->owned = 1.  Errors: OEC_ERR_ARG (NULL/invalid), OEC_ERR_CUDA (allocation). */
+oec_status oec_field_create(const int64_t domain[3], const int32_t halo_lo[3], const int32_t halo_hi[3],
+                            int32_t dtype, int32_t device, const int32_t order[3], int32_t k_invariant,
+                            oec_field *out);
+
+/* Describe caller-owned memory (e.g. a torch tensor) as a field; out->owned = 0.  No copy, no
+ * allocation.  Errors: OEC_ERR_ARG, OEC_ERR_LAYOUT (stride[0] != 1, stride[2] == 0 without
+ * ub[2]-lb[2] == 1). */
+oec_status oec_field_wrap(void *data, const int64_t lb[3], const int64_t ub[3], const int64_t stride[3],
+                          int32_t dtype, int32_t device, oec_field *out);
+
+/* Free the memory of an owned field (no-op for borrowed ones) and clear the descriptor. */
+oec_status oec_field_destroy(oec_field *f);
+
+/* ----------------------------------------------------------------------------------------- */
+/* Program registry: names, argument order and access extents (a1, shape inference P:480).     */
+/* ----------------------------------------------------------------------------------------- */
+/* Programs: "hdiff", "vadv", "uvbke", "p_grad_c", "nh_p_grad", "fvtp2d_qi", "fvtp2d_qj",
+ * "fvtp2d_flux", "fastwaves" (Table II P:575-580 + north_star).  n_* may be NULL. */
+oec_status oec_program_info(const char *program, int32_t *n_inputs, int32_t *n_outputs, int32_t *n_scalars);
+
+/* Input `idx` of `program`: its name (static string), its access extent relative to the
+ * domain -- the input must cover [dom_lb + lo, dom_ub + hi) -- and whether it is a k-invariant
+ * (2D) field.  lo[d] <= 0 <= hi[d].  (vadv's wcon: lo = {0,0,0}, hi = {1,0,0}.) */
+oec_status oec_program_input(const char *program, int32_t idx, const char **name, int64_t lo[3], int64_t hi[3],
+                             int32_t *k_invariant);
+
+/* Name of output `idx` / scalar `idx` (static strings). */
+oec_status oec_program_output(const char *program, int32_t idx, const char **name);
+oec_status oec_program_scalar(const char *program, int32_t idx, const char **name, double *default_value);
+
+/* ----------------------------------------------------------------------------------------- */
+/* The hot path.                                                                              */
+/* ----------------------------------------------------------------------------------------- */
+
+/* hdiff -- COSMO horizontal diffusion (north_star; PAPER.md has no definition, R1-R6):
+ *   lap = ((in[i-1]+in[i+1]) + (in[j-1]+in[j+1])) - 4 in
+ *   flx = f*(in[i+1]-in) > 0 ? 0 : f,  f = lap[i+1]-lap        (flux limiter, select)
+ *   fly = g*(in[j+1]-in) > 0 ? 0 : g,  g = lap[j+1]-lap
+ *   out = in - coeff*((flx - flx[i-1]) + (fly - fly[j-1]))
+ * in: extent i,j in [-2,+2], k 0 (13-point diamond); coeff: the output point only.
+ * One fused kernel; lap/flx/fly never touch HBM. */
+oec_status oec_hdiff(const oec_field *in, const oec_field *coeff, oec_field *out, const int64_t dom_lb[3],
+                     const int64_t dom_ub[3], void *stream);
+
+/* Same with an explicit oec_variant. */
+oec_status oec_hdiff_variant(const oec_field *in, const oec_field *coeff, oec_field *out, const int64_t dom_lb[3],
+                             const int64_t dom_ub[3], int32_t variant, void *stream);
+
+/* vadv -- vertical advection: per column (i,j) the tridiagonal system
+ *   a_k x_{k-1} + b_k x_k + c_k x_{k+1} = d_k,  k = dom_lb[2] .. dom_ub[2]-1,
+ * solved by the Thomas algorithm ("Some use the Thomas algorithm to perform implicit
+ * integration in the vertical direction"); coefficients from u_stage and wcon
+ * (BET_M = BET_P = 0.5), d from u_pos, utens, utens_stage_in; out = dtr_stage*(x - u_pos).
+ * Full definition: DESIGN.md R7-R11.  wcon extent i in [0,+1]; all others the point only.
+ * K = dom_ub[2]-dom_lb[2] >= 2 else OEC_ERR_SHAPE.  One fused kernel; c', d' stay on chip. */
+oec_status oec_vadv(const oec_field *u_stage, const oec_field *wcon, const oec_field *u_pos, const oec_field *utens,
+                    const oec_field *utens_stage_in, oec_field *utens_stage_out, double dtr_stage,
+                    const int64_t dom_lb[3], const int64_t dom_ub[3], void *stream);
+
+/* Apply any registered program (incl. hdiff and vadv).  inputs/outputs in registry order
+ * (oec_program_input/output), scalars in registry order (NULL/n_scalars = 0: defaults).
+ * variant: oec_variant.  Errors as above; OEC_ERR_ARG for wrong counts / unknown program. */
+oec_status oec_apply_program(const char *program, const oec_field *const *inputs, int32_t n_inputs,
+                             oec_field *const *outputs, int32_t n_outputs, const double *scalars, int32_t n_scalars,
+                             const int64_t dom_lb[3], const int64_t dom_ub[3], int32_t variant, void *stream);
+
+/* Number of kernel launches the last successful oec_* compute call on this thread enqueued
+ * (bench.py's gpu_launches count). */
+int32_t oec_last_launch_count(void);
+
+/* ----------------------------------------------------------------------------------------- */
+/* Horizontal domain decomposition + halo exchange (a8; north_star (3)).  Not in PAPER.md. */
+/* ----------------------------------------------------------------------------------------- */
+typedef struct oec_decomp oec_decomp; /* opaque */
+
+/* One halo message of a rank: copy the box [lo, hi) of a field between this rank and `peer`
+ * (send: from our interior; recv: into our halo).  Boxes are absolute GLOBAL coordinates. */
+typedef struct oec_halo_msg {
+    int32_t peer;   /* rank                                                 */
+    int32_t is_send;/* 1 = send our box to peer, 0 = receive peer's into it */
+    int32_t phase;  /* 0 = i-phase, 1 = j-phase (corners ride in phase 1)    */
+    int32_t tag;
+    int64_t lo[3];
+    int64_t hi[3];
+} oec_halo_msg;
+
+/* Split global_domain over px * py ranks (i split px ways, j split py ways, k never split --
+ * the vadv recurrence is sequential in k); rank r sits at (r % px, r / px).  Blocks differ in
+ * size by at most one cell.  local_lb/ub (may be NULL): this rank's sub-domain in GLOBAL
+ * coordinates.  nccl_comm: an ncclComm_t (e.g. torch ProcessGroupNCCL._comm_ptr()) used by
+ * oec_halo_exchange, or NULL for plan-only use (oec_decomp_plan).  The library resolves NCCL
+ * from the process (the copy torch already loaded) at the first exchange. */
+oec_status oec_decomp_create(const int64_t global_domain[3], int32_t px, int32_t py, int32_t rank, void *nccl_comm,
+                             oec_decomp **out, int64_t local_lb[3], int64_t local_ub[3]);
+
+/* The messages rank `rank` exchanges for a halo of widths width_lo/width_hi (i, j; k ignored)
+ * around its sub-domain, in execution order: phase 0 (i-neighbours, j-range of the interior)
+ * then phase 1 (j-neighbours, i-range INCLUDING the i-halo, so corners are filled).  Non-periodic
+ * global boundary: nothing is exchanged across it.  *n_msgs = the number of messages; at most
+ * `capacity` are written to `msgs` (msgs may be NULL to query the count). */
+oec_status oec_decomp_plan(const oec_decomp *d, const int32_t width_lo[3], const int32_t width_hi[3],
+                           oec_halo_msg *msgs, int32_t capacity, int32_t *n_msgs);
+
+/* Exchange the halos of n device fields with the neighbouring ranks over NCCL (send/recv
+ * groups over NVLink/NVSwitch), enqueued on `stream`.  Each field is described in the rank's
+ * LOCAL coordinates (origin = the rank's sub-domain lower bound local_lb, exactly like a
+ * single-GPU field of that sub-domain) and must cover the sub-domain grown by the widths.
+ * Boxes are packed/unpacked by liboec kernels around the NCCL calls.  Errors: OEC_ERR_NCCL when
+ * no communicator / NCCL unavailable, OEC_ERR_SHAPE when a field does not cover the halo. */
+oec_status oec_halo_exchange(oec_decomp *d, oec_field *const *fields, int32_t n, const int32_t width_lo[3],
+                             const int32_t width_hi[3], void *stream);
+
+/* Same exchange executed on ONE device between sub-domain fields of all ranks
+ * (fields[r * n + f] = field f of rank r, in rank r's local coordinates): device-to-device box
+ * copies driven by the same plan, phase 0 for all ranks before phase 1.
+ * Used to test decomposition logic on a single GPU. */
+oec_status oec_halo_exchange_local(const int64_t global_domain[3], int32_t px, int32_t py, oec_field *const *fields,
+                                   int32_t n, const int32_t width_lo[3], const int32_t width_hi[3], void *stream);
+
+oec_status oec_decomp_destroy(oec_decomp *d);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* OEC_H */

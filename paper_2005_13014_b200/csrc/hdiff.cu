@@ -1,0 +1,289 @@
+// hdiff -- COSMO horizontal diffusion, fused into one pass over HBM (stencil inlining, P:431;
+// "we do not need to store and load any temporary buffer").  Definition: include/oec.h,
+// DESIGN.md readings R1-R6.  Built with --fmad=false: every + - * below rounds separately, in the
+// parenthesised order of the definition, so results equal the CPU oracle bit for bit.
+//
+// Two kernels:
+//  * hdiff_naive  -- the paper's execution model: one thread per grid point, every
+//                    producer inlined and recomputed, all temporaries in registers, no shared
+//                    memory, no synchronisation.  13 `in` loads per point go through L1.
+//  * hdiff_roll   -- B200 design: a warp owns a W = 32*V wide i-segment
+//                    of one k-plane and walks a chunk of JB rows along j.  Each `in` row is loaded
+//                    once (coalesced, 16-byte vectors when aligned) plus a 2-wide halo on each side,
+//                    extended to i-2..i+V+1 per lane with warp shuffles, and rolled through
+//                    registers: lap, flx and fly are recomputed per lane from registers (no L1
+//                    re-reads, no shared memory, no barriers).  P rows of `in` and `coeff` are kept
+//                    in flight per warp (software prefetch) for memory-level parallelism.
+#include "oec_internal.h"
+
+namespace oec {
+namespace {
+
+__device__ __forceinline__ double ld(const FV &f, int i, int j, int k) { return __ldg(f.p + (i + j * f.sj + k * f.sk)); }
+
+__device__ __forceinline__ double lap_pt(double c, double w, double e, double s, double n) {
+    // lap(i,j) = ((in(i-1,j) + in(i+1,j)) + (in(i,j-1) + in(i,j+1))) - 4 in(i,j)
+    return ((w + e) + (s + n)) - 4.0 * c;
+}
+__device__ __forceinline__ double limit(double f, double din) { return (f * din > 0.0) ? 0.0 : f; }
+
+// ---------------------------------------------------------------------------------------------
+// paper execution model
+// ---------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(128) hdiff_naive(FV in, FV coeff, FO out, Dom d) {
+    const int i = d.lo[0] + blockIdx.x * 32 + threadIdx.x;
+    const int j = d.lo[1] + blockIdx.y * 4 + threadIdx.y;
+    const int k = d.lo[2] + blockIdx.z;
+    if (i >= d.hi[0] || j >= d.hi[1]) return;
+    auto L = [&](int a, int b) {
+        return lap_pt(ld(in, a, b, k), ld(in, a - 1, b, k), ld(in, a + 1, b, k), ld(in, a, b - 1, k), ld(in, a, b + 1, k));
+    };
+    const double c0 = ld(in, i, j, k);
+    const double l0 = L(i, j), le = L(i + 1, j), lw = L(i - 1, j), ln = L(i, j + 1), ls = L(i, j - 1);
+    const double flx = limit(le - l0, ld(in, i + 1, j, k) - c0);
+    const double flxm = limit(l0 - lw, c0 - ld(in, i - 1, j, k));
+    const double fly = limit(ln - l0, ld(in, i, j + 1, k) - c0);
+    const double flym = limit(l0 - ls, c0 - ld(in, i, j - 1, k));
+    out.p[i + j * out.sj + k * out.sk] = c0 - ld(coeff, i, j, k) * ((flx - flxm) + (fly - flym));
+}
+
+// ---------------------------------------------------------------------------------------------
+// rolling kernel
+// ---------------------------------------------------------------------------------------------
+template <int V>
+struct Vec;
+template <>
+struct Vec<1> {
+    static __device__ __forceinline__ void load(const double *p, double *v) { v[0] = __ldg(p); }
+    static __device__ __forceinline__ void store(double *p, const double *v) { p[0] = v[0]; }
+};
+template <>
+struct Vec<2> {
+    static __device__ __forceinline__ void load(const double *p, double *v) {
+        double2 t = __ldg(reinterpret_cast<const double2 *>(p));
+        v[0] = t.x;
+        v[1] = t.y;
+    }
+    static __device__ __forceinline__ void store(double *p, const double *v) {
+        *reinterpret_cast<double2 *>(p) = make_double2(v[0], v[1]);
+    }
+};
+
+// raw row as loaded: V own values + (lane 0) 2 left-halo values + (lane 31) 2 right-halo values
+template <int V>
+struct RawRow {
+    double v[V];
+    double h[2];
+};
+
+template <int V>
+__device__ __forceinline__ void load_row(const double *rowp, int i_own, int lane, int i_end_in, int ib, RawRow<V> &r) {
+    // rowp: pointer to element (0, j, k); i_own = ib + lane*V; valid `in` columns: i < i_end_in
+    if (i_own + V <= i_end_in) {
+        Vec<V>::load(rowp + i_own, r.v);
+    } else {
+#pragma unroll
+        for (int v = 0; v < V; ++v) r.v[v] = (i_own + v < i_end_in) ? __ldg(rowp + i_own + v) : 0.0;
+    }
+    r.h[0] = r.h[1] = 0.0;
+    if (lane == 0) {
+        r.h[0] = __ldg(rowp + ib - 2);
+        r.h[1] = __ldg(rowp + ib - 1);
+    } else if (lane == 31) {
+        const int ir = ib + 32 * V;
+        if (ir < i_end_in) r.h[0] = __ldg(rowp + ir);
+        if (ir + 1 < i_end_in) r.h[1] = __ldg(rowp + ir + 1);
+    }
+}
+
+// extended row: e[x + 2] = in(i_own + x), x in [-2, V+1]
+template <int V>
+__device__ __forceinline__ void extend(const RawRow<V> &r, int lane, double *e) {
+    constexpr unsigned FULL = 0xffffffffu;
+#pragma unroll
+    for (int v = 0; v < V; ++v) e[v + 2] = r.v[v];
+    double l1, l2, r1, r2;
+    if (V >= 2) {
+        l2 = __shfl_up_sync(FULL, r.v[V - 2 < 0 ? 0 : V - 2], 1);
+        l1 = __shfl_up_sync(FULL, r.v[V - 1], 1);
+        r1 = __shfl_down_sync(FULL, r.v[0], 1);
+        r2 = __shfl_down_sync(FULL, r.v[V >= 2 ? 1 : 0], 1);
+    } else {
+        l2 = __shfl_up_sync(FULL, r.v[0], 2);
+        l1 = __shfl_up_sync(FULL, r.v[0], 1);
+        r1 = __shfl_down_sync(FULL, r.v[0], 1);
+        r2 = __shfl_down_sync(FULL, r.v[0], 2);
+    }
+    if (V == 1) {  // lanes 0/1 and 30/31 take the halo for the parts outside the warp
+        if (lane == 1) l2 = __shfl_sync(FULL, r.h[1], 0);
+        else __shfl_sync(FULL, r.h[1], 0);
+        if (lane == 30) r2 = __shfl_sync(FULL, r.h[0], 31);
+        else __shfl_sync(FULL, r.h[0], 31);
+    }
+    if (lane == 0) {
+        l2 = r.h[0];
+        l1 = r.h[1];
+    }
+    if (lane == 31) {
+        r1 = r.h[0];
+        r2 = r.h[1];
+    }
+    e[0] = l2;
+    e[1] = l1;
+    e[V + 2] = r1;
+    e[V + 3] = r2;
+}
+
+template <int V, int JB, int P>
+__global__ void __launch_bounds__(128) hdiff_roll(FV in, FV coeff, FO out, Dom d, int nseg, int nchunk) {
+    constexpr int W = 32 * V;
+    const int lane = threadIdx.x & 31;
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int seg = warp % nseg;
+    const int chunk = (warp / nseg) % nchunk;
+    const int k = d.lo[2] + warp / (nseg * nchunk);
+    if (k >= d.hi[2]) return;  // whole warp exits together
+    const int ib = d.lo[0] + seg * W;
+    const int i_own = ib + lane * V;
+    const int i_end_in = d.hi[0] + 2;  // `in` columns needed: [ib-2, min(ib+W, hi0)+2)
+    const int j0 = d.lo[1] + chunk * JB;
+    const int j1 = min(j0 + JB, d.hi[1]);
+    const double *in_k = in.p + k * in.sk;
+    const double *cf_k = coeff.p + k * coeff.sk;
+    double *out_k = out.p + k * out.sk;
+
+    double E0[V + 4], E1[V + 4], E2[V + 4];  // in rows j, j+1, j+2 (extended)
+    double Lj[V + 2];                        // lap row j at i_own-1 .. i_own+V
+    double FYm[V];                           // fly(j-1) at own points
+
+    // ---- warm-up: rows j0-2 .. j0+1 ----
+    {
+        RawRow<V> r;
+        double Em2[V + 4], Em1[V + 4];
+        load_row<V>(in_k + (j0 - 2) * in.sj, i_own, lane, i_end_in, ib, r);
+        extend<V>(r, lane, Em2);
+        load_row<V>(in_k + (j0 - 1) * in.sj, i_own, lane, i_end_in, ib, r);
+        extend<V>(r, lane, Em1);
+        load_row<V>(in_k + j0 * in.sj, i_own, lane, i_end_in, ib, r);
+        extend<V>(r, lane, E0);
+        load_row<V>(in_k + (j0 + 1) * in.sj, i_own, lane, i_end_in, ib, r);
+        extend<V>(r, lane, E1);
+        double Lm[V];  // lap(j0-1) at own points
+#pragma unroll
+        for (int x = 0; x < V; ++x) Lm[x] = lap_pt(Em1[x + 2], Em1[x + 1], Em1[x + 3], Em2[x + 2], E0[x + 2]);
+#pragma unroll
+        for (int y = 0; y < V + 2; ++y)  // lap(j0) at i_own + y - 1
+            Lj[y] = lap_pt(E0[y + 1], E0[y], E0[y + 2], Em1[y + 1], E1[y + 1]);
+#pragma unroll
+        for (int x = 0; x < V; ++x) FYm[x] = limit(Lj[x + 1] - Lm[x], E0[x + 2] - Em1[x + 2]);
+    }
+
+    // ---- prefetch ring: slot s holds in row (j+2) and coeff row j for step j = j0 + s (mod P) ----
+    RawRow<V> ring_in[P];
+    double ring_cf[P][V];
+    const bool own_valid = i_own < d.hi[0];
+#pragma unroll
+    for (int s = 0; s < P; ++s) {
+        const int j = j0 + s;
+        if (j < j1) {
+            load_row<V>(in_k + (j + 2) * in.sj, i_own, lane, i_end_in, ib, ring_in[s]);
+            if (own_valid) {
+                if (i_own + V <= d.hi[0]) Vec<V>::load(cf_k + j * coeff.sj + i_own, ring_cf[s]);
+                else {
+#pragma unroll
+                    for (int v = 0; v < V; ++v) ring_cf[s][v] = (i_own + v < d.hi[0]) ? __ldg(cf_k + j * coeff.sj + i_own + v) : 0.0;
+                }
+            }
+        }
+    }
+
+    for (int jb = j0; jb < j1; jb += P) {
+#pragma unroll
+        for (int s = 0; s < P; ++s) {
+            const int j = jb + s;
+            if (j < j1) {  // warp-uniform
+                extend<V>(ring_in[s], lane, E2);
+                double cf[V];
+#pragma unroll
+                for (int v = 0; v < V; ++v) cf[v] = ring_cf[s][v];
+                // refill this slot with step j + P
+                const int jn = j + P;
+                if (jn < j1) {
+                    load_row<V>(in_k + (jn + 2) * in.sj, i_own, lane, i_end_in, ib, ring_in[s]);
+                    if (own_valid) {
+                        if (i_own + V <= d.hi[0]) Vec<V>::load(cf_k + jn * coeff.sj + i_own, ring_cf[s]);
+                        else {
+#pragma unroll
+                            for (int v = 0; v < V; ++v)
+                                ring_cf[s][v] = (i_own + v < d.hi[0]) ? __ldg(cf_k + jn * coeff.sj + i_own + v) : 0.0;
+                        }
+                    }
+                }
+                // lap(j+1) at i_own-1 .. i_own+V
+                double L1[V + 2];
+#pragma unroll
+                for (int y = 0; y < V + 2; ++y) L1[y] = lap_pt(E1[y + 1], E1[y], E1[y + 2], E0[y + 1], E2[y + 1]);
+                // flx(j) at i_own-1 .. i_own+V-1:  FX[y] <-> i_own + y - 1
+                double FX[V + 1];
+#pragma unroll
+                for (int y = 0; y < V + 1; ++y) FX[y] = limit(Lj[y + 1] - Lj[y], E0[y + 2] - E0[y + 1]);
+                // fly(j) at own points
+                double FY[V];
+#pragma unroll
+                for (int x = 0; x < V; ++x) FY[x] = limit(L1[x + 1] - Lj[x + 1], E1[x + 2] - E0[x + 2]);
+                double o[V];
+#pragma unroll
+                for (int x = 0; x < V; ++x) o[x] = E0[x + 2] - cf[x] * ((FX[x + 1] - FX[x]) + (FY[x] - FYm[x]));
+                if (own_valid) {
+                    double *op = out_k + j * out.sj + i_own;
+                    if (i_own + V <= d.hi[0]) Vec<V>::store(op, o);
+                    else {
+#pragma unroll
+                        for (int v = 0; v < V; ++v)
+                            if (i_own + v < d.hi[0]) op[v] = o[v];
+                    }
+                }
+                // roll
+#pragma unroll
+                for (int y = 0; y < V + 4; ++y) {
+                    E0[y] = E1[y];
+                    E1[y] = E2[y];
+                }
+#pragma unroll
+                for (int y = 0; y < V + 2; ++y) Lj[y] = L1[y];
+#pragma unroll
+                for (int x = 0; x < V; ++x) FYm[x] = FY[x];
+            }
+        }
+    }
+}
+
+template <int V, int JB, int P>
+cudaError_t launch_roll(const FV &in, const FV &coeff, const FO &out, const Dom &d, cudaStream_t s, int *launches) {
+    constexpr int W = 32 * V;
+    const int ni = d.hi[0] - d.lo[0], nj = d.hi[1] - d.lo[1], nk = d.hi[2] - d.lo[2];
+    const int nseg = (ni + W - 1) / W, nchunk = (nj + JB - 1) / JB;
+    const long long warps = (long long)nseg * nchunk * nk;
+    const int threads = 128;
+    const long long blocks = (warps * 32 + threads - 1) / threads;
+    hdiff_roll<V, JB, P><<<(unsigned)blocks, threads, 0, s>>>(in, coeff, out, d, nseg, nchunk);
+    ++*launches;
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_hdiff(const FV &in, const FV &coeff, const FO &out, const Dom &d, int variant, bool aligned16,
+                         cudaStream_t s, int *launches) {
+    if (variant == OEC_VARIANT_NAIVE) {
+        dim3 block(32, 4, 1);
+        dim3 grid((d.hi[0] - d.lo[0] + 31) / 32, (d.hi[1] - d.lo[1] + 3) / 4, d.hi[2] - d.lo[2]);
+        hdiff_naive<<<grid, block, 0, s>>>(in, coeff, out, d);
+        ++*launches;
+        return cudaGetLastError();
+    }
+    if (aligned16) return launch_roll<2, 16, 4>(in, coeff, out, d, s, launches);
+    return launch_roll<1, 16, 4>(in, coeff, out, d, s, launches);
+}
+
+}  // namespace oec

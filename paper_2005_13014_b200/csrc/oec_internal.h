@@ -1,0 +1,62 @@
+// Internal declarations of liboec (not part of the ABI; see include/oec.h).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/oec.h"
+
+namespace oec {
+
+// A field as the kernels see it: a pointer to the ORIGIN element (0,0,0) -- possibly outside
+// the allocation, only ever dereferenced at validated in-range offsets -- and 32-bit element
+// strides (the host checks every reachable offset fits in int32; "integer index
+// computations are a significant performance bottleneck").
+struct FV {
+    const double *p;
+    int32_t sj, sk;  // sk == 0 for k-invariant fields
+};
+struct FO {
+    double *p;
+    int32_t sj, sk;
+};
+
+// Domain of one launch: [lo, hi) in absolute coordinates.
+struct Dom {
+    int32_t lo[3], hi[3];
+};
+
+// launchers (return cudaGetLastError() of their launches); `launches` is incremented per launch
+cudaError_t launch_hdiff(const FV &in, const FV &coeff, const FO &out, const Dom &d, int variant, bool aligned16,
+                         cudaStream_t s, int *launches);
+cudaError_t launch_vadv(const FV &u_stage, const FV &wcon, const FV &u_pos, const FV &utens, const FV &usi,
+                        const FO &out, double dtr, const Dom &d, cudaStream_t s, int *launches);
+// suite: inputs / outputs in registry order
+cudaError_t launch_suite(int program_id, const FV *in, const FO *out, const double *scalars, const Dom &d,
+                         cudaStream_t s, int *launches);
+
+// box copies for halo exchange: [lo, hi) box (absolute coords) between fields / packed buffers
+struct Box {
+    int32_t lo[3], hi[3];
+};
+cudaError_t launch_pack(const FV &src, const Box &b, double *buf, cudaStream_t s, int *launches);
+cudaError_t launch_unpack(const double *buf, const Box &b, const FO &dst, cudaStream_t s, int *launches);
+cudaError_t launch_box_copy(const FV &src, const FO &dst, const Box &b, cudaStream_t s, int *launches);
+
+// error plumbing
+oec_status set_error(oec_status st, const char *fmt, ...);
+
+}  // namespace oec
+
+// program ids (registry order in runtime.cpp)
+enum {
+    OEC_PROG_HDIFF = 0,
+    OEC_PROG_VADV = 1,
+    OEC_PROG_UVBKE = 2,
+    OEC_PROG_P_GRAD_C = 3,
+    OEC_PROG_NH_P_GRAD = 4,
+    OEC_PROG_FVTP2D_QI = 5,
+    OEC_PROG_FVTP2D_QJ = 6,
+    OEC_PROG_FVTP2D_FLUX = 7,
+    OEC_PROG_FASTWAVES = 8,
+    OEC_NPROG = 9
+};

@@ -1,0 +1,616 @@
+// liboec host runtime: field descriptors, program registry (access extents), validation,
+// host staging for the end-to-end path, and dispatch to the sm_100a kernels.
+//
+// Registry extents are shape inference (§5.2) done once by hand per program:
+// the minimal bounding box of every access of every inlined operator.  tests/test_abi_host.py
+// checks them against the oracle's brute-force touched-index trace.
+#include <cuda_runtime.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <mutex>
+#include <vector>
+
+#include "oec_internal.h"
+
+namespace oec {
+
+static thread_local char g_err[1024];
+static thread_local int g_launches;
+
+oec_status set_error(oec_status st, const char *fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof g_err, fmt, ap);
+    va_end(ap);
+    return st;
+}
+
+// ---------------------------------------------------------------------------------------------
+// program registry
+// ---------------------------------------------------------------------------------------------
+struct InSpec {
+    const char *name;
+    int lo[3], hi[3];  // access extent relative to the domain
+    int k_invariant;
+};
+struct ScSpec {
+    const char *name;
+    double dflt;
+};
+struct ProgSpec {
+    const char *name;
+    int n_in, n_out, n_sc;
+    InSpec in[9];
+    const char *out[3];
+    ScSpec sc[2];
+};
+
+#define Z3 {0, 0, 0}
+static const ProgSpec PROGS[OEC_NPROG] = {
+    {"hdiff", 2, 1, 0, {{"in", {-2, -2, 0}, {2, 2, 0}, 0}, {"coeff", Z3, Z3, 0}}, {"out"}, {}},
+    {"vadv",
+     5,
+     1,
+     1,
+     {{"u_stage", Z3, Z3, 0},
+      {"wcon", Z3, {1, 0, 0}, 0},
+      {"u_pos", Z3, Z3, 0},
+      {"utens", Z3, Z3, 0},
+      {"utens_stage_in", Z3, Z3, 0}},
+     {"utens_stage_out"},
+     {{"dtr_stage", 3.0 / 20.0}}},
+    {"uvbke",
+     4,
+     2,
+     1,
+     {{"uc", {0, -1, 0}, Z3, 0}, {"vc", {-1, 0, 0}, Z3, 0}, {"cosa", Z3, Z3, 1}, {"rsina", Z3, Z3, 1}},
+     {"ub", "vb"},
+     {{"dt5", 0.5 * 225.0 / 1000.0}}},
+    {"p_grad_c",
+     7,
+     2,
+     1,
+     {{"uc", Z3, Z3, 0},
+      {"vc", Z3, Z3, 0},
+      {"delpc", {-1, -1, 0}, Z3, 0},
+      {"pkc", {-1, -1, 0}, {0, 0, 1}, 0},
+      {"gz", {-1, -1, 0}, {0, 0, 1}, 0},
+      {"rdxc", Z3, Z3, 1},
+      {"rdyc", Z3, Z3, 1}},
+     {"uc_out", "vc_out"},
+     {{"dt2", 0.5 * 225.0 / 1000.0}}},
+    {"nh_p_grad",
+     8,
+     2,
+     1,
+     {{"u", Z3, Z3, 0},
+      {"v", Z3, Z3, 0},
+      {"pp", Z3, {1, 1, 1}, 0},
+      {"gz", Z3, {1, 1, 1}, 0},
+      {"pk3", Z3, {1, 1, 1}, 0},
+      {"delp", Z3, {1, 1, 0}, 0},
+      {"rdx", Z3, Z3, 1},
+      {"rdy", Z3, Z3, 1}},
+     {"u_out", "v_out"},
+     {{"dt", 225.0 / 1000.0}}},
+    {"fvtp2d_qi",
+     5,
+     2,
+     0,
+     {{"q", {0, -3, 0}, {0, 3, 0}, 0},
+      {"cry", Z3, {0, 1, 0}, 0},
+      {"yfx", Z3, {0, 1, 0}, 0},
+      {"area", Z3, Z3, 1},
+      {"ra_y", Z3, Z3, 0}},
+     {"q_i", "fy2"},
+     {}},
+    {"fvtp2d_qj",
+     6,
+     3,
+     0,
+     {{"q", {-3, 0, 0}, {3, 0, 0}, 0},
+      {"q_i", {-3, 0, 0}, {2, 0, 0}, 0},
+      {"crx", Z3, {1, 0, 0}, 0},
+      {"xfx", Z3, {1, 0, 0}, 0},
+      {"area", Z3, Z3, 1},
+      {"ra_x", Z3, Z3, 0}},
+     {"q_j", "fx", "fx2"},
+     {}},
+    {"fvtp2d_flux",
+     7,
+     2,
+     0,
+     {{"q_j", {0, -3, 0}, {0, 2, 0}, 0},
+      {"cry", Z3, Z3, 0},
+      {"fx", Z3, Z3, 0},
+      {"fx2", Z3, Z3, 0},
+      {"fy2", Z3, Z3, 0},
+      {"mfx", Z3, Z3, 0},
+      {"mfy", Z3, Z3, 0}},
+     {"fx_out", "fy_out"},
+     {}},
+    {"fastwaves",
+     9,
+     2,
+     2,
+     {{"u_pos", Z3, Z3, 0},
+      {"v_pos", Z3, Z3, 0},
+      {"u_tens", Z3, Z3, 0},
+      {"v_tens", Z3, Z3, 0},
+      {"rho", Z3, {1, 1, 0}, 0},
+      {"ppuv", {0, 0, -1}, {1, 1, 1}, 0},
+      {"fx", Z3, Z3, 1},
+      {"wgtfac", Z3, {1, 1, 1}, 0},
+      {"hhl", Z3, {1, 1, 1}, 0}},
+     {"u_out", "v_out"},
+     {{"edadlat", 0.25}, {"dt", 10.0 / 1000.0}}},
+};
+
+static int find_prog(const char *name) {
+    if (!name) return -1;
+    for (int p = 0; p < OEC_NPROG; ++p)
+        if (strcmp(PROGS[p].name, name) == 0) return p;
+    return -1;
+}
+
+// ---------------------------------------------------------------------------------------------
+// validation
+// ---------------------------------------------------------------------------------------------
+static bool span_bytes(const oec_field *f, uintptr_t *lo, uintptr_t *hi) {
+    // byte range [lo, hi) spanned by the allocation of f
+    int64_t mn = 0, mx = 0;
+    for (int d = 0; d < 3; ++d) {
+        int64_t n = f->ub[d] - f->lb[d];
+        if (n <= 0) return false;
+        int64_t e = (n - 1) * f->stride[d];
+        if (e < 0) mn += e; else mx += e;
+    }
+    *lo = (uintptr_t)f->data + (uintptr_t)(mn * 8);
+    *hi = (uintptr_t)f->data + (uintptr_t)((mx + 1) * 8);
+    return true;
+}
+
+static oec_status check_field(const oec_field *f, const char *what, int *device) {
+    if (!f || !f->data) return set_error(OEC_ERR_ARG, "%s: NULL field or data pointer", what);
+    if (f->dtype != OEC_F64) return set_error(OEC_ERR_DTYPE, "%s: dtype %d is not OEC_F64", what, f->dtype);
+    if (*device == -2) *device = f->device;
+    else if (*device != f->device)
+        return set_error(OEC_ERR_DTYPE, "%s: device %d differs from the other fields' device %d", what, f->device,
+                         *device);
+    if (f->stride[0] != 1) return set_error(OEC_ERR_LAYOUT, "%s: stride[0] = %lld, must be 1", what, (long long)f->stride[0]);
+    for (int d = 0; d < 3; ++d)
+        if (f->ub[d] <= f->lb[d]) return set_error(OEC_ERR_SHAPE, "%s: empty allocation in dim %d", what, d);
+    if (((uintptr_t)f->data) % 8) return set_error(OEC_ERR_LAYOUT, "%s: data not 8-byte aligned", what);
+    return OEC_OK;
+}
+
+static bool is_k_invariant(const oec_field *f) { return f->stride[2] == 0 && f->ub[2] - f->lb[2] == 1 && f->lb[2] == 0; }
+
+// make the kernel view; checks every allocated element is reachable with int32 offsets from the origin
+template <class V>
+static oec_status make_view(const oec_field *f, const char *what, V *v) {
+    int64_t sj = f->stride[1], sk = is_k_invariant(f) ? 0 : f->stride[2];
+    if (sj > INT32_MAX || sk > INT32_MAX || sj < INT32_MIN || sk < INT32_MIN)
+        return set_error(OEC_ERR_LAYOUT, "%s: stride exceeds int32", what);
+    int64_t lbk = is_k_invariant(f) ? 0 : f->lb[2];
+    int64_t origin_off = -(f->lb[0] + f->lb[1] * sj + lbk * sk);  // element offset of (0,0,0) from data
+    for (int c = 0; c < 8; ++c) {
+        int64_t i = (c & 1) ? f->ub[0] - 1 : f->lb[0];
+        int64_t j = (c & 2) ? f->ub[1] - 1 : f->lb[1];
+        int64_t k = (c & 4) ? f->ub[2] - 1 : f->lb[2];
+        int64_t off = i + j * sj + k * sk;
+        if (off > INT32_MAX || off < INT32_MIN)
+            return set_error(OEC_ERR_LAYOUT, "%s: element offsets exceed int32 (field too large for this build)", what);
+    }
+    v->p = (decltype(v->p))((char *)f->data + origin_off * 8);
+    v->sj = (int32_t)sj;
+    v->sk = (int32_t)sk;
+    return OEC_OK;
+}
+
+static oec_status check_domain(const int64_t *lo, const int64_t *hi) {
+    if (!lo || !hi) return set_error(OEC_ERR_ARG, "NULL domain");
+    for (int d = 0; d < 3; ++d) {
+        if (hi[d] < lo[d]) return set_error(OEC_ERR_SHAPE, "domain dim %d: ub %lld < lb %lld", d, (long long)hi[d], (long long)lo[d]);
+        if (lo[d] < INT32_MIN / 2 || hi[d] > INT32_MAX / 2) return set_error(OEC_ERR_LAYOUT, "domain bounds exceed int32");
+    }
+    return OEC_OK;
+}
+
+static bool domain_empty(const int64_t *lo, const int64_t *hi) {
+    return hi[0] <= lo[0] || hi[1] <= lo[1] || hi[2] <= lo[2];
+}
+
+static oec_status check_cover(const oec_field *f, const char *what, const int64_t *lo, const int64_t *hi,
+                              const int *elo, const int *ehi, int k_inv) {
+    if (k_inv && !is_k_invariant(f))
+        return set_error(OEC_ERR_SHAPE, "%s: must be a k-invariant (2D) field: lb[2]=0, ub[2]=1, stride[2]=0", what);
+    for (int d = 0; d < 3; ++d) {
+        if (d == 2 && is_k_invariant(f)) continue;
+        int64_t need_lo = lo[d] + elo[d], need_hi = hi[d] + ehi[d];
+        if (f->lb[d] > need_lo || f->ub[d] < need_hi)
+            return set_error(OEC_ERR_SHAPE,
+                             "%s: allocation [%lld,%lld) in dim %d does not cover the accessed range [%lld,%lld) "
+                             "(domain + access extent, P:482)",
+                             what, (long long)f->lb[d], (long long)f->ub[d], d, (long long)need_lo, (long long)need_hi);
+    }
+    return OEC_OK;
+}
+
+// ---------------------------------------------------------------------------------------------
+// host staging (end-to-end path, device == OEC_DEVICE_HOST)
+// ---------------------------------------------------------------------------------------------
+struct Staging {
+    std::mutex mu;
+    std::vector<void *> bufs;
+    std::vector<size_t> sizes;
+    int device = -1;
+};
+static Staging g_stage;
+
+static oec_status stage_buffer(size_t idx, size_t bytes, void **p) {
+    if (g_stage.bufs.size() <= idx) {
+        g_stage.bufs.resize(idx + 1, nullptr);
+        g_stage.sizes.resize(idx + 1, 0);
+    }
+    if (g_stage.sizes[idx] < bytes) {
+        if (g_stage.bufs[idx]) cudaFree(g_stage.bufs[idx]);
+        g_stage.bufs[idx] = nullptr;
+        g_stage.sizes[idx] = 0;
+        cudaError_t e = cudaMalloc(&g_stage.bufs[idx], bytes);
+        if (e != cudaSuccess) return set_error(OEC_ERR_CUDA, "staging cudaMalloc(%zu): %s", bytes, cudaGetErrorString(e));
+        g_stage.sizes[idx] = bytes;
+    }
+    *p = g_stage.bufs[idx];
+    return OEC_OK;
+}
+
+// copy the domain box of a strided device field back into the same-layout host field
+static cudaError_t d2h_box(const oec_field *host, const oec_field *dev, const int64_t *lo, const int64_t *hi,
+                           cudaStream_t s) {
+    // outer loop over the dimension with the larger stride, 2D copies over the other two
+    int outer = (host->stride[2] >= host->stride[1]) ? 2 : 1;
+    int mid = 3 - outer;
+    int64_t w = (hi[0] - lo[0]) * 8;
+    for (int64_t o = lo[outer]; o < hi[outer]; ++o) {
+        int64_t idx[3] = {lo[0], 0, 0};
+        idx[outer] = o;
+        idx[mid] = lo[mid];
+        int64_t off = (idx[0] - host->lb[0]) + (idx[1] - host->lb[1]) * host->stride[1] +
+                      (is_k_invariant(host) ? 0 : (idx[2] - host->lb[2]) * host->stride[2]);
+        cudaError_t e = cudaMemcpy2DAsync((char *)host->data + off * 8, host->stride[mid] * 8,
+                                          (char *)dev->data + off * 8, dev->stride[mid] * 8, w, hi[mid] - lo[mid],
+                                          cudaMemcpyDeviceToHost, s);
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+}
+
+// ---------------------------------------------------------------------------------------------
+// dispatch
+// ---------------------------------------------------------------------------------------------
+static oec_status run_device(int p, const oec_field *const *in, oec_field *const *out, const double *sc,
+                             const int64_t *lo, const int64_t *hi, int variant, cudaStream_t s) {
+    const ProgSpec &P = PROGS[p];
+    FV v_in[9];
+    FO v_out[3];
+    bool aligned16 = true;
+    for (int q = 0; q < P.n_in; ++q) {
+        oec_status st = make_view(in[q], P.in[q].name, &v_in[q]);
+        if (st) return st;
+        aligned16 = aligned16 && ((uintptr_t)v_in[q].p % 16 == 0) && (v_in[q].sj % 2 == 0) && (v_in[q].sk % 2 == 0);
+    }
+    for (int q = 0; q < P.n_out; ++q) {
+        oec_status st = make_view(out[q], P.out[q], &v_out[q]);
+        if (st) return st;
+        aligned16 = aligned16 && ((uintptr_t)v_out[q].p % 16 == 0) && (v_out[q].sj % 2 == 0) && (v_out[q].sk % 2 == 0);
+    }
+    Dom d;
+    for (int q = 0; q < 3; ++q) {
+        d.lo[q] = (int32_t)lo[q];
+        d.hi[q] = (int32_t)hi[q];
+    }
+    aligned16 = aligned16 && (d.lo[0] % 2 == 0);
+    int launches = 0;
+    cudaError_t e;
+    switch (p) {
+    case OEC_PROG_HDIFF: e = launch_hdiff(v_in[0], v_in[1], v_out[0], d, variant, aligned16, s, &launches); break;
+    case OEC_PROG_VADV:
+        e = launch_vadv(v_in[0], v_in[1], v_in[2], v_in[3], v_in[4], v_out[0], sc[0], d, s, &launches);
+        break;
+    default: e = launch_suite(p, v_in, v_out, sc, d, s, &launches); break;
+    }
+    if (e != cudaSuccess) return set_error(OEC_ERR_CUDA, "%s: kernel launch failed: %s", P.name, cudaGetErrorString(e));
+    g_launches = launches;
+    return OEC_OK;
+}
+
+static oec_status apply(int p, const oec_field *const *in, int n_in, oec_field *const *out, int n_out,
+                        const double *scalars, int n_sc, const int64_t *lo, const int64_t *hi, int variant,
+                        void *stream) {
+    const ProgSpec &P = PROGS[p];
+    g_err[0] = 0;
+    g_launches = 0;
+    if (n_in != P.n_in || n_out != P.n_out)
+        return set_error(OEC_ERR_ARG, "%s: expects %d inputs / %d outputs, got %d / %d", P.name, P.n_in, P.n_out, n_in, n_out);
+    if (!in || !out) return set_error(OEC_ERR_ARG, "%s: NULL input/output array", P.name);
+    if (n_sc != 0 && n_sc != P.n_sc) return set_error(OEC_ERR_ARG, "%s: expects %d scalars, got %d", P.name, P.n_sc, n_sc);
+    if (n_sc && !scalars) return set_error(OEC_ERR_ARG, "%s: NULL scalars", P.name);
+    if (variant != OEC_VARIANT_AUTO && variant != OEC_VARIANT_NAIVE)
+        return set_error(OEC_ERR_ARG, "%s: unknown variant %d", P.name, variant);
+    oec_status st = check_domain(lo, hi);
+    if (st) return st;
+    int device = -2;
+    for (int q = 0; q < P.n_in; ++q)
+        if ((st = check_field(in[q], P.in[q].name, &device))) return st;
+    for (int q = 0; q < P.n_out; ++q)
+        if ((st = check_field(out[q], P.out[q], &device))) return st;
+    for (int q = 0; q < P.n_out; ++q)
+        if (is_k_invariant(out[q]))
+            return set_error(OEC_ERR_SHAPE, "%s: output %s must not be k-invariant", P.name, P.out[q]);
+    if (p == OEC_PROG_VADV && hi[2] - lo[2] < 2)
+        return set_error(OEC_ERR_SHAPE, "vadv: K = %lld < 2 (the k=0 and k=K-1 rows would coincide)", (long long)(hi[2] - lo[2]));
+    static const int Z[3] = {0, 0, 0};
+    bool empty = domain_empty(lo, hi);
+    if (!empty) {
+        for (int q = 0; q < P.n_in; ++q)
+            if ((st = check_cover(in[q], P.in[q].name, lo, hi, P.in[q].lo, P.in[q].hi, P.in[q].k_invariant))) return st;
+        for (int q = 0; q < P.n_out; ++q)
+            if ((st = check_cover(out[q], P.out[q], lo, hi, Z, Z, 0))) return st;
+    }
+    // aliasing: an output may not overlap any input or another output
+    for (int q = 0; q < P.n_out; ++q) {
+        uintptr_t a0, a1;
+        span_bytes(out[q], &a0, &a1);
+        for (int r = 0; r < P.n_in; ++r) {
+            uintptr_t b0, b1;
+            span_bytes(in[r], &b0, &b1);
+            if (a0 < b1 && b0 < a1)
+                return set_error(OEC_ERR_ALIAS, "%s: output %s overlaps input %s (P:381 alias-free parameters)", P.name,
+                                 P.out[q], P.in[r].name);
+        }
+        for (int r = 0; r < q; ++r) {
+            uintptr_t b0, b1;
+            span_bytes(out[r], &b0, &b1);
+            if (a0 < b1 && b0 < a1)
+                return set_error(OEC_ERR_ALIAS, "%s: outputs %s and %s overlap", P.name, P.out[q], P.out[r]);
+        }
+    }
+    double sc[2];
+    for (int q = 0; q < P.n_sc; ++q) sc[q] = n_sc ? scalars[q] : P.sc[q].dflt;
+    if (empty) return OEC_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+
+    if (device >= 0) return run_device(p, in, out, sc, lo, hi, variant, s);
+    if (device != OEC_DEVICE_HOST) return set_error(OEC_ERR_ARG, "%s: invalid device %d", P.name, device);
+
+    // ---- end-to-end path: stage host fields through cached device buffers ----
+    std::lock_guard<std::mutex> lock(g_stage.mu);
+    oec_field din[9], dout[3];
+    const oec_field *pin[9];
+    oec_field *pout[3];
+    size_t slot = 0;
+    for (int q = 0; q < P.n_in; ++q) {
+        uintptr_t b0, b1;
+        span_bytes(in[q], &b0, &b1);
+        void *dptr;
+        if ((st = stage_buffer(slot++, b1 - b0, &dptr))) return st;
+        din[q] = *in[q];
+        din[q].device = 0;
+        din[q].data = (char *)dptr + ((uintptr_t)in[q]->data - b0);
+        cudaError_t e = cudaMemcpyAsync(dptr, (const void *)b0, b1 - b0, cudaMemcpyHostToDevice, s);
+        if (e != cudaSuccess) return set_error(OEC_ERR_CUDA, "H2D copy of %s: %s", P.in[q].name, cudaGetErrorString(e));
+        pin[q] = &din[q];
+    }
+    for (int q = 0; q < P.n_out; ++q) {
+        uintptr_t b0, b1;
+        span_bytes(out[q], &b0, &b1);
+        void *dptr;
+        if ((st = stage_buffer(slot++, b1 - b0, &dptr))) return st;
+        dout[q] = *out[q];
+        dout[q].device = 0;
+        dout[q].data = (char *)dptr + ((uintptr_t)out[q]->data - b0);
+        pout[q] = &dout[q];
+    }
+    if ((st = run_device(p, pin, pout, sc, lo, hi, variant, s))) return st;
+    int launches = g_launches;
+    for (int q = 0; q < P.n_out; ++q) {
+        cudaError_t e = d2h_box(out[q], &dout[q], lo, hi, s);
+        if (e != cudaSuccess) return set_error(OEC_ERR_CUDA, "D2H copy of %s: %s", P.out[q], cudaGetErrorString(e));
+    }
+    cudaError_t e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return set_error(OEC_ERR_CUDA, "%s: %s", P.name, cudaGetErrorString(e));
+    g_launches = launches;
+    return OEC_OK;
+}
+
+}  // namespace oec
+
+using namespace oec;
+
+extern "C" {
+
+int32_t oec_abi_version(void) { return OEC_ABI_VERSION; }
+
+const char *oec_build_info(void) {
+    return "liboec: sm_100a, fp64, --fmad=false, kernels: hdiff(rolling-j register/shuffle, naive), vadv(thomas, "
+           "register-prefetch, smem c'/d'), suite(inlined per-point), halo(pack/unpack, NCCL send/recv)";
+}
+
+const char *oec_last_error(void) { return g_err; }
+
+int32_t oec_last_launch_count(void) { return g_launches; }
+
+oec_status oec_field_create(const int64_t domain[3], const int32_t halo_lo[3], const int32_t halo_hi[3], int32_t dtype,
+                            int32_t device, const int32_t order[3], int32_t k_invariant, oec_field *out) {
+    g_err[0] = 0;
+    if (!domain || !halo_lo || !halo_hi || !out) return set_error(OEC_ERR_ARG, "oec_field_create: NULL argument");
+    if (dtype != OEC_F64) return set_error(OEC_ERR_DTYPE, "oec_field_create: dtype %d unsupported", dtype);
+    if (device < 0) return set_error(OEC_ERR_ARG, "oec_field_create: device %d must be a CUDA ordinal", device);
+    for (int d = 0; d < 3; ++d)
+        if (domain[d] < 1 || halo_lo[d] < 0 || halo_hi[d] < 0)
+            return set_error(OEC_ERR_ARG, "oec_field_create: domain >= 1 and halos >= 0 required");
+    if (halo_lo[0] > 16) return set_error(OEC_ERR_ARG, "oec_field_create: i halo_lo %d > 16 (the left pad)", halo_lo[0]);
+    if (k_invariant && (domain[2] != 1 || halo_lo[2] || halo_hi[2]))
+        return set_error(OEC_ERR_ARG, "oec_field_create: k_invariant requires domain[2] == 1 and no k halo");
+    int ord[3] = {0, 2, 1};
+    if (order) {
+        bool seen[3] = {false, false, false};
+        for (int d = 0; d < 3; ++d) {
+            if (order[d] < 0 || order[d] > 2 || seen[order[d]])
+                return set_error(OEC_ERR_ARG, "oec_field_create: order is not a permutation");
+            seen[order[d]] = true;
+            ord[d] = order[d];
+        }
+        if (ord[0] != 0) return set_error(OEC_ERR_LAYOUT, "oec_field_create: i must be the fastest dimension");
+    }
+    // i: 16-element left pad (i = 0 is 128-byte aligned), pitch a multiple of 16 elements
+    int64_t n[3];
+    n[0] = 16 + domain[0] + halo_hi[0];
+    n[0] = (n[0] + 15) / 16 * 16;
+    n[1] = domain[1] + halo_lo[1] + halo_hi[1];
+    n[2] = domain[2] + halo_lo[2] + halo_hi[2];
+    int64_t stride[3];
+    stride[ord[0]] = 1;
+    stride[ord[1]] = n[ord[0]];
+    stride[ord[2]] = n[ord[0]] * n[ord[1]];
+    size_t bytes = (size_t)(n[0] * n[1] * n[2]) * 8;
+    int prev;
+    cudaGetDevice(&prev);
+    cudaSetDevice(device);
+    void *base = nullptr;
+    cudaError_t e = cudaMalloc(&base, bytes);
+    if (e == cudaSuccess) e = cudaMemset(base, 0, bytes);
+    cudaSetDevice(prev);
+    if (e != cudaSuccess) return set_error(OEC_ERR_CUDA, "oec_field_create: %s", cudaGetErrorString(e));
+    memset(out, 0, sizeof *out);
+    out->lb[0] = -halo_lo[0];
+    out->lb[1] = -halo_lo[1];
+    out->lb[2] = -halo_lo[2];
+    out->ub[0] = domain[0] + halo_hi[0];
+    out->ub[1] = domain[1] + halo_hi[1];
+    out->ub[2] = domain[2] + halo_hi[2];
+    out->stride[0] = 1;
+    out->stride[1] = stride[1];
+    out->stride[2] = k_invariant ? 0 : stride[2];
+    // data points at (lb0, lb1, lb2): the row starts 16 - halo_lo[0] elements into the pad
+    out->data = (char *)base + (16 - halo_lo[0]) * 8;
+    out->dtype = dtype;
+    out->device = device;
+    out->owned = 1;
+    return OEC_OK;
+}
+
+oec_status oec_field_wrap(void *data, const int64_t lb[3], const int64_t ub[3], const int64_t stride[3], int32_t dtype,
+                          int32_t device, oec_field *out) {
+    g_err[0] = 0;
+    if (!data || !lb || !ub || !stride || !out) return set_error(OEC_ERR_ARG, "oec_field_wrap: NULL argument");
+    if (dtype != OEC_F64) return set_error(OEC_ERR_DTYPE, "oec_field_wrap: dtype %d unsupported", dtype);
+    if (stride[0] != 1) return set_error(OEC_ERR_LAYOUT, "oec_field_wrap: stride[0] must be 1");
+    for (int d = 0; d < 3; ++d)
+        if (ub[d] <= lb[d]) return set_error(OEC_ERR_ARG, "oec_field_wrap: empty range in dim %d", d);
+    if (stride[2] == 0 && !(lb[2] == 0 && ub[2] == 1))
+        return set_error(OEC_ERR_LAYOUT, "oec_field_wrap: stride[2] == 0 requires lb[2]=0, ub[2]=1");
+    memset(out, 0, sizeof *out);
+    out->data = data;
+    for (int d = 0; d < 3; ++d) {
+        out->lb[d] = lb[d];
+        out->ub[d] = ub[d];
+        out->stride[d] = stride[d];
+    }
+    out->dtype = dtype;
+    out->device = device;
+    out->owned = 0;
+    return OEC_OK;
+}
+
+oec_status oec_field_destroy(oec_field *f) {
+    g_err[0] = 0;
+    if (!f) return set_error(OEC_ERR_ARG, "oec_field_destroy: NULL");
+    if (f->owned && f->data) {
+        void *base = (char *)f->data - (16 + f->lb[0]) * 8;
+        int prev;
+        cudaGetDevice(&prev);
+        cudaSetDevice(f->device);
+        cudaError_t e = cudaFree(base);
+        cudaSetDevice(prev);
+        if (e != cudaSuccess) return set_error(OEC_ERR_CUDA, "oec_field_destroy: %s", cudaGetErrorString(e));
+    }
+    memset(f, 0, sizeof *f);
+    return OEC_OK;
+}
+
+oec_status oec_program_info(const char *program, int32_t *n_inputs, int32_t *n_outputs, int32_t *n_scalars) {
+    int p = find_prog(program);
+    if (p < 0) return set_error(OEC_ERR_ARG, "unknown program '%s'", program ? program : "(null)");
+    if (n_inputs) *n_inputs = PROGS[p].n_in;
+    if (n_outputs) *n_outputs = PROGS[p].n_out;
+    if (n_scalars) *n_scalars = PROGS[p].n_sc;
+    return OEC_OK;
+}
+
+oec_status oec_program_input(const char *program, int32_t idx, const char **name, int64_t lo[3], int64_t hi[3],
+                             int32_t *k_invariant) {
+    int p = find_prog(program);
+    if (p < 0) return set_error(OEC_ERR_ARG, "unknown program '%s'", program ? program : "(null)");
+    if (idx < 0 || idx >= PROGS[p].n_in) return set_error(OEC_ERR_ARG, "%s: input index %d out of range", program, idx);
+    const InSpec &s = PROGS[p].in[idx];
+    if (name) *name = s.name;
+    for (int d = 0; d < 3; ++d) {
+        if (lo) lo[d] = s.lo[d];
+        if (hi) hi[d] = s.hi[d];
+    }
+    if (k_invariant) *k_invariant = s.k_invariant;
+    return OEC_OK;
+}
+
+oec_status oec_program_output(const char *program, int32_t idx, const char **name) {
+    int p = find_prog(program);
+    if (p < 0) return set_error(OEC_ERR_ARG, "unknown program '%s'", program ? program : "(null)");
+    if (idx < 0 || idx >= PROGS[p].n_out) return set_error(OEC_ERR_ARG, "%s: output index %d out of range", program, idx);
+    if (name) *name = PROGS[p].out[idx];
+    return OEC_OK;
+}
+
+oec_status oec_program_scalar(const char *program, int32_t idx, const char **name, double *default_value) {
+    int p = find_prog(program);
+    if (p < 0) return set_error(OEC_ERR_ARG, "unknown program '%s'", program ? program : "(null)");
+    if (idx < 0 || idx >= PROGS[p].n_sc) return set_error(OEC_ERR_ARG, "%s: scalar index %d out of range", program, idx);
+    if (name) *name = PROGS[p].sc[idx].name;
+    if (default_value) *default_value = PROGS[p].sc[idx].dflt;
+    return OEC_OK;
+}
+
+oec_status oec_hdiff_variant(const oec_field *in, const oec_field *coeff, oec_field *out, const int64_t dom_lb[3],
+                             const int64_t dom_ub[3], int32_t variant, void *stream) {
+    const oec_field *ins[2] = {in, coeff};
+    oec_field *outs[1] = {out};
+    return apply(OEC_PROG_HDIFF, ins, 2, outs, 1, nullptr, 0, dom_lb, dom_ub, variant, stream);
+}
+
+oec_status oec_hdiff(const oec_field *in, const oec_field *coeff, oec_field *out, const int64_t dom_lb[3],
+                     const int64_t dom_ub[3], void *stream) {
+    return oec_hdiff_variant(in, coeff, out, dom_lb, dom_ub, OEC_VARIANT_AUTO, stream);
+}
+
+oec_status oec_vadv(const oec_field *u_stage, const oec_field *wcon, const oec_field *u_pos, const oec_field *utens,
+                    const oec_field *utens_stage_in, oec_field *utens_stage_out, double dtr_stage,
+                    const int64_t dom_lb[3], const int64_t dom_ub[3], void *stream) {
+    const oec_field *ins[5] = {u_stage, wcon, u_pos, utens, utens_stage_in};
+    oec_field *outs[1] = {utens_stage_out};
+    return apply(OEC_PROG_VADV, ins, 5, outs, 1, &dtr_stage, 1, dom_lb, dom_ub, OEC_VARIANT_AUTO, stream);
+}
+
+oec_status oec_apply_program(const char *program, const oec_field *const *inputs, int32_t n_inputs,
+                             oec_field *const *outputs, int32_t n_outputs, const double *scalars, int32_t n_scalars,
+                             const int64_t dom_lb[3], const int64_t dom_ub[3], int32_t variant, void *stream) {
+    g_err[0] = 0;
+    int p = find_prog(program);
+    if (p < 0) return set_error(OEC_ERR_ARG, "unknown program '%s'", program ? program : "(null)");
+    return apply(p, inputs, n_inputs, outputs, n_outputs, scalars, n_scalars, dom_lb, dom_ub, variant, stream);
+}
+
+}  // extern "C"

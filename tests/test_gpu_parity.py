@@ -1,0 +1,203 @@
+"""GPU parity: the CUDA path (through the C-ABI) vs the CPU oracle, element by element, on the
+same seeded inputs.  Bar (BASELINE.json north_star): per-element max relative
+error <= 1e-12 in fp64; the kernels are built to be bit-identical, so we also require zero bit
+differences; domain-boundary / halo indexing bit-exact; output halos never written."""
+import numpy as np
+import pytest
+
+import synth
+from gpu_util import SENTINEL, compare, domain_part, outside_mask, run_gpu, run_oracle
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-12
+ORDERS = [None, (0, 1, 2)]  # default i,k,j and i,j,k
+
+
+def _assert_parity(g, r, what):
+    c = compare(g, r)
+    assert c["max_rel"] <= TOL and c["zero_ok"], (what, c)
+    assert c["n_bitdiff"] == 0, (what, c)
+    assert not np.isnan(g).any(), what
+
+
+def _check(program, domain, seed=0, order=None, variant=0, dom_lb=(0, 0, 0), dom_ub=None, out_halo=(0, 0, 0)):
+    host = synth.make_inputs(program, domain, seed=seed)
+    dom_ub = dom_ub or domain
+    g = run_gpu(program, host, domain, order=order, variant=variant, dom_lb=dom_lb, dom_ub=dom_ub, out_halo=out_halo)
+    r = run_oracle(program, host, domain, dom_lb=dom_lb, dom_ub=dom_ub)
+    for name in synth.PROGRAMS[program].outputs:
+        _assert_parity(domain_part(g[name], dom_lb, dom_ub), r[name], (program, name, domain, seed, order))
+        assert np.all(g[name].data[outside_mask(g[name], dom_lb, dom_ub)] == SENTINEL), (program, name, "wrote outside")
+
+
+@pytest.mark.parametrize("seed", range(5))
+@pytest.mark.parametrize("program", ["hdiff", "vadv"])
+def test_config0_all_seeds(program, seed):
+    # BASELINE.json configs[0]: 32x32x16, halo 2; parity seeds {0..4}
+    _check(program, (32, 32, 16), seed=seed)
+
+
+@pytest.mark.parametrize("order", ORDERS)
+@pytest.mark.parametrize("program", synth.ALL_PROGRAMS)
+def test_ragged_both_layouts(program, order):
+    # non-divisible sizes exercise the predicated tails (reading R15); output halo 2 holds a sentinel
+    _check(program, (33, 31, 5), seed=1, order=order, out_halo=(2, 2, 1))
+
+
+@pytest.mark.parametrize("program", synth.ALL_PROGRAMS)
+def test_several_tiles(program):
+    _check(program, (200, 70, 9), seed=2)
+
+
+@pytest.mark.parametrize("program", synth.ALL_PROGRAMS)
+def test_degenerate_tiny(program):
+    _check(program, (1, 1, 2), seed=3)
+    if program != "vadv":
+        _check(program, (1, 1, 1), seed=3)
+        _check(program, (2, 3, 1), seed=3)
+
+
+@pytest.mark.parametrize("program", synth.ALL_PROGRAMS)
+def test_subdomain_call(program):
+    # dom_lb/dom_ub select a sub-range (P:336 absolute ranges): only it is written
+    _check(program, (40, 24, 6), seed=4, dom_lb=(3, 5, 1), dom_ub=(35, 19, 5), out_halo=(0, 0, 0))
+
+
+@pytest.mark.parametrize("program", synth.ALL_PROGRAMS)
+def test_paper_config_full_compare(program):
+    # BASELINE.json configs[1] / configs[2]: 128x128x80, the oracle over the whole domain
+    _check(program, (128, 128, 80), seed=0)
+
+
+def test_hdiff_naive_variant():
+    for dom in [(32, 32, 16), (33, 31, 5), (128, 128, 8)]:
+        _check("hdiff", dom, seed=0, variant=2)
+
+
+def test_hdiff_smooth_input():
+    domain = (128, 64, 4)
+    host = synth.make_inputs("hdiff", domain, seed=0, smooth=True)
+    g = run_gpu("hdiff", host, domain)
+    r = run_oracle("hdiff", host, domain)
+    _assert_parity(domain_part(g["out"], (0, 0, 0), domain), r["out"], "smooth")
+
+
+@pytest.mark.parametrize("order", ORDERS)
+def test_hdiff_integer_probe_is_exact(order):
+    # integer-coded probe in = i + 2^10 j + 2^20 k (exact in fp64, linear -> lap = 0): every access
+    # offset that is wrong would change the output; out must equal in bit for bit
+    domain = (70, 19, 3)
+    host = synth.make_inputs("hdiff", domain, seed=0)
+    host["in"] = synth.probe_field(host["in"].lb, host["in"].ub)
+    g = run_gpu("hdiff", host, domain, order=order)
+    exp = domain_part(host["in"], (0, 0, 0), domain)
+    assert np.array_equal(domain_part(g["out"], (0, 0, 0), domain), exp)
+
+
+@pytest.mark.parametrize("program", synth.ALL_PROGRAMS)
+def test_nan_canaries_outside_touched_set(program):
+    # NaN in every allocated input cell the program does not read (brute-force trace): no NaN may
+    # reach an output (no stray reads influence results)
+    from oracle import stencil as st
+    from oracle import suite
+
+    domain = (37, 9, 4)
+    host = synth.make_inputs(program, domain, seed=5)
+    if program != "vadv":
+        _, touched = st.run_fused(suite.PROGRAMS[program], host, synth.scalars(program), (0, 0, 0), domain)
+    else:
+        touched = None
+    for s in synth.PROGRAMS[program].inputs:
+        f = host[s.name]
+        if touched is not None:
+            keep = np.zeros(f.data.shape, bool)
+            for (i, j, k) in touched[s.name]:
+                keep[k - f.lb[2], j - f.lb[1], i - f.lb[0]] = True
+        else:  # vadv: wcon level k0 is allocated but never read
+            keep = np.ones(f.data.shape, bool)
+            if s.name == "wcon":
+                keep[0] = False
+        f.data[~keep] = np.nan
+    g = run_gpu(program, host, domain)
+    r = run_oracle(program, host, domain)
+    for name in synth.PROGRAMS[program].outputs:
+        _assert_parity(domain_part(g[name], (0, 0, 0), domain), r[name], (program, name, "canary"))
+
+
+def test_mutation_is_detected():
+    # the harness must fail on an off-by-one offset: compare the GPU against the
+    # oracle run on `in` shifted by one in i
+    domain = (32, 16, 2)
+    host = synth.make_inputs("hdiff", domain, seed=0)
+    g = run_gpu("hdiff", host, domain)
+    shifted = {k: v.copy() for k, v in host.items()}
+    shifted["in"].data[:, :, :-1] = host["in"].data[:, :, 1:]
+    r = run_oracle("hdiff", shifted, domain)
+    c = compare(domain_part(g["out"], (0, 0, 0), domain), r["out"])
+    assert c["max_rel"] > TOL and c["n_bitdiff"] > 0
+
+
+@pytest.mark.parametrize("program", ["hdiff", "vadv", "fvtp2d_qj"])
+def test_host_buffers_end_to_end(program):
+    # device = OEC_DEVICE_HOST: the library stages H2D, runs, copies the domain back (e2e path)
+    from paper_2005_13014_b200 import oec
+
+    domain = (48, 20, 6)
+    host = synth.make_inputs(program, domain, seed=6)
+    spec = synth.PROGRAMS[program]
+    ins = [oec.oec_field_wrap(host[s.name].data, host[s.name].lb, host[s.name].ub, k_invariant=s.k_invariant)
+           for s in spec.inputs]
+    outs_np = [np.full((domain[2] + 2, domain[1] + 2, domain[0] + 2), SENTINEL) for _ in spec.outputs]
+    outs = [oec.oec_field_wrap(a, (-1, -1, -1), (domain[0] + 1, domain[1] + 1, domain[2] + 1)) for a in outs_np]
+    oec.oec_apply_program(program, ins, outs, None, (0, 0, 0), domain)
+    r = run_oracle(program, host, domain)
+    for name, a in zip(spec.outputs, outs_np):
+        assert np.array_equal(a[1:-1, 1:-1, 1:-1], r[name]), (program, name)
+        m = np.ones(a.shape, bool)
+        m[1:-1, 1:-1, 1:-1] = False
+        assert np.all(a[m] == SENTINEL)
+
+
+def test_alias_rejected_on_device():
+    from paper_2005_13014_b200 import oec
+
+    domain = (16, 16, 2)
+    host = synth.make_inputs("hdiff", domain, seed=0)
+    inp = oec.field_from_host(host["in"])
+    cf = oec.field_from_host(host["coeff"])
+    with pytest.raises(oec.OecError) as e:
+        oec.oec_hdiff(inp, cf, cf, (0, 0, 0), domain)
+    assert e.value.status == 3
+
+
+def test_torch_wrapped_fields():
+    # fields wrapping plain torch tensors (the caller's memory, owned=0), contiguous [k][j][i]
+    import torch
+
+    from paper_2005_13014_b200 import oec
+
+    domain = (50, 30, 7)
+    host = synth.make_inputs("hdiff", domain, seed=7)
+    t_in = torch.from_numpy(host["in"].data).cuda()
+    t_cf = torch.from_numpy(host["coeff"].data).cuda()
+    t_out = torch.full((7, 30, 50), float("nan"), dtype=torch.float64, device="cuda")
+    oec.oec_hdiff(oec.oec_field_wrap(t_in, host["in"].lb, host["in"].ub),
+                  oec.oec_field_wrap(t_cf, (0, 0, 0), domain), oec.oec_field_wrap(t_out, (0, 0, 0), domain),
+                  (0, 0, 0), domain)
+    torch.cuda.synchronize()
+    r = run_oracle("hdiff", host, domain)
+    _assert_parity(t_out.cpu().numpy(), r["out"], "torch-wrapped (odd pitch, V=1 path)")
+
+
+@pytest.mark.parametrize("program", ["hdiff", "vadv"])
+def test_full_size_sampled(program):
+    # BASELINE.json configs[3]: 1024x1024x80 in the launch configuration bench.py times; the
+    # oracle on sampled sub-boxes (hdiff) / column blocks (vadv) it finishes in seconds
+    domain = (1024, 1024, 80)
+    host = synth.make_inputs(program, domain, seed=0)
+    g = run_gpu(program, host, domain)
+    name = synth.PROGRAMS[program].outputs[0]
+    for lo, hi in [((0, 0, 0), (64, 48, 80)), ((960, 976, 0), (1024, 1024, 80)), ((500, 300, 0), (580, 340, 80))]:
+        r = run_oracle(program, host, domain, dom_lb=lo, dom_ub=hi)
+        _assert_parity(domain_part(g[name], lo, hi), r[name], (program, lo, hi))
