@@ -3,7 +3,16 @@
 // DESIGN.md readings R1-R6.  Built with --fmad=false: every + - * below rounds separately, in the
 // parenthesised order of the definition, so results equal the CPU oracle bit for bit.
 //
-// Two kernels:
+// Three kernels:
+//  * hdiff_tma    -- default B200 design: persistent CTAs of NW
+//                    independent warps; each warp owns an S-deep ring of shared-memory slots fed by
+//                    TMA (cp.async.bulk.tensor, mbarrier complete_tx).  A work item is a W x JB tile
+//                    of one k-plane: one TMA box of `in` ((W+4) x (JB+4), halo included, OOB
+//                    zero-filled) and one of `coeff` (W x JB).  The warp walks the tile along j,
+//                    each lane reading its V columns plus the 2-wide halo straight from shared
+//                    memory (16-byte LDS, conflict-free) and rolling lap/flx/fly in registers.
+//                    The bytes in flight live in the TMA ring, not in registers, so ~S items per
+//                    warp are always streaming from HBM while the warp computes.
 //  * hdiff_naive  -- the paper's execution model: one thread per grid point, every
 //                    producer inlined and recomputed, all temporaries in registers, no shared
 //                    memory, no synchronisation.  13 `in` loads per point go through L1.
@@ -14,7 +23,23 @@
 //                    registers: lap, flx and fly are recomputed per lane from registers (no L1
 //                    re-reads, no shared memory, no barriers).  P rows of `in` and `coeff` are kept
 //                    in flight per warp (software prefetch) for memory-level parallelism.
+#include <algorithm>
+
 #include "oec_internal.h"
+#include "tma.h"
+
+#ifndef HD_V
+#define HD_V 2
+#endif
+#ifndef HD_JB
+#define HD_JB 8
+#endif
+#ifndef HD_S
+#define HD_S 3
+#endif
+#ifndef HD_NW
+#define HD_NW 6
+#endif
 
 namespace oec {
 namespace {
@@ -69,6 +94,18 @@ struct Vec<2> {
     }
 };
 
+template <>
+struct Vec<4> {
+    static __device__ __forceinline__ void load(const double *p, double *v) {
+        Vec<2>::load(p, v);
+        Vec<2>::load(p + 2, v + 2);
+    }
+    static __device__ __forceinline__ void store(double *p, const double *v) {
+        Vec<2>::store(p, v);
+        Vec<2>::store(p + 2, v + 2);
+    }
+};
+
 // raw row as loaded: V own values + (lane 0) 2 left-halo values + (lane 31) 2 right-halo values
 template <int V>
 struct RawRow {
@@ -114,11 +151,11 @@ __device__ __forceinline__ void extend(const RawRow<V> &r, int lane, double *e) 
         r1 = __shfl_down_sync(FULL, r.v[0], 1);
         r2 = __shfl_down_sync(FULL, r.v[0], 2);
     }
-    if (V == 1) {  // lanes 0/1 and 30/31 take the halo for the parts outside the warp
-        if (lane == 1) l2 = __shfl_sync(FULL, r.h[1], 0);
-        else __shfl_sync(FULL, r.h[1], 0);
-        if (lane == 30) r2 = __shfl_sync(FULL, r.h[0], 31);
-        else __shfl_sync(FULL, r.h[0], 31);
+    if (V == 1) {  // lanes 1 and 30 take the halo values held by lanes 0 and 31
+        const double hl = __shfl_sync(FULL, r.h[1], 0);
+        const double hr = __shfl_sync(FULL, r.h[0], 31);
+        if (lane == 1) l2 = hl;
+        if (lane == 30) r2 = hr;
     }
     if (lane == 0) {
         l2 = r.h[0];
@@ -258,6 +295,174 @@ __global__ void __launch_bounds__(128) hdiff_roll(FV in, FV coeff, FO out, Dom d
     }
 }
 
+// ---------------------------------------------------------------------------------------------
+// TMA-fed kernel
+// ---------------------------------------------------------------------------------------------
+template <int V, int JB, int S, int NW>
+struct TmaCfg {
+    static constexpr int W = 32 * V;
+    static constexpr int IN_ELEMS = (JB + 4) * (W + 4);
+    static constexpr int IN_BYTES = IN_ELEMS * 8;
+    static constexpr int CF_BYTES = JB * W * 8;
+    static constexpr int IN_PAD = (IN_BYTES + 127) / 128 * 128;
+    static constexpr int CF_PAD = (CF_BYTES + 127) / 128 * 128;
+    static constexpr int SLOT = IN_PAD + CF_PAD;
+    static constexpr int SMEM = NW * S * SLOT + NW * S * 8;
+};
+
+template <int V>
+__device__ __forceinline__ void lds_row(const double *row, int lane, double *e) {
+    // e[x] = row[lane*V + x], x in [0, V+4)  (row element x <-> i = ib - 2 + x)
+    const double *p = row + lane * V;
+    if constexpr (V % 2 == 0) {
+#pragma unroll
+        for (int x = 0; x < V + 4; x += 2) {
+            const double2 t = *reinterpret_cast<const double2 *>(p + x);
+            e[x] = t.x;
+            e[x + 1] = t.y;
+        }
+    } else {
+#pragma unroll
+        for (int x = 0; x < V + 4; ++x) e[x] = p[x];
+    }
+}
+
+template <int V, int JB, int S, int NW>
+__global__ void __launch_bounds__(NW * 32, 1) hdiff_tma(const __grid_constant__ TMap m_in, const __grid_constant__ TMap m_cf,
+                                                     FO out, Dom d, int nseg, int nchunk, int nitems) {
+    using C = TmaCfg<V, JB, S, NW>;
+    constexpr int W = C::W;
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    unsigned char *wbase = smem + warp * S * C::SLOT;
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + NW * S * C::SLOT) + warp * S;
+    const int gw = blockIdx.x * NW + warp, nwt = gridDim.x * NW;
+
+    auto in_s = [&](int s) { return reinterpret_cast<double *>(wbase + s * C::SLOT); };
+    auto cf_s = [&](int s) { return reinterpret_cast<double *>(wbase + s * C::SLOT + C::IN_PAD); };
+    auto decode = [&](int item, int &ib, int &j0, int &k) {
+        const int seg = item % nseg, chunk = (item / nseg) % nchunk;
+        k = d.lo[2] + item / (nseg * nchunk);
+        ib = d.lo[0] + seg * W;
+        j0 = d.lo[1] + chunk * JB;
+    };
+    auto issue = [&](int item, int s) {
+        int ib, j0, k;
+        decode(item, ib, j0, k);
+        mbar_expect_tx(&bars[s], C::IN_BYTES + C::CF_BYTES);
+        tma_load_ijk(in_s(s), m_in, &bars[s], ib - 2, j0 - 2, k);
+        tma_load_ijk(cf_s(s), m_cf, &bars[s], ib, j0, k);
+    };
+
+    if (lane == 0) {
+        prefetch_tmap(&m_in.map);
+        prefetch_tmap(&m_cf.map);
+#pragma unroll
+        for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
+        fence_mbar_init();
+#pragma unroll
+        for (int s = 0; s < S; ++s)
+            if (gw + s * nwt < nitems) issue(gw + s * nwt, s);
+    }
+    __syncwarp();
+
+    int n = 0;
+    for (int item = gw; item < nitems; item += nwt, ++n) {
+        const int s = n % S;
+        mbar_wait(&bars[s], (n / S) & 1);
+        int ib, j0, k;
+        decode(item, ib, j0, k);
+        const int j1 = min(j0 + JB, d.hi[1]);
+        const int i_own = ib + lane * V;
+        const bool own_valid = i_own < d.hi[0];
+        const double *tin = in_s(s);
+        const double *tcf = cf_s(s);
+        double *out_k = out.p + k * out.sk;
+
+        double E0[V + 4], E1[V + 4], E2[V + 4], Lj[V + 2], FYm[V];
+        {
+            double Em2[V + 4], Em1[V + 4], Lm[V];
+            lds_row<V>(tin + 0 * (W + 4), lane, Em2);
+            lds_row<V>(tin + 1 * (W + 4), lane, Em1);
+            lds_row<V>(tin + 2 * (W + 4), lane, E0);
+            lds_row<V>(tin + 3 * (W + 4), lane, E1);
+#pragma unroll
+            for (int x = 0; x < V; ++x) Lm[x] = lap_pt(Em1[x + 2], Em1[x + 1], Em1[x + 3], Em2[x + 2], E0[x + 2]);
+#pragma unroll
+            for (int y = 0; y < V + 2; ++y) Lj[y] = lap_pt(E0[y + 1], E0[y], E0[y + 2], Em1[y + 1], E1[y + 1]);
+#pragma unroll
+            for (int x = 0; x < V; ++x) FYm[x] = limit(Lj[x + 1] - Lm[x], E0[x + 2] - Em1[x + 2]);
+        }
+#pragma unroll 2
+        for (int r = 0; r < JB; ++r) {
+            const int j = j0 + r;
+            if (j >= j1) break;  // warp-uniform
+            lds_row<V>(tin + (r + 4) * (W + 4), lane, E2);
+            double L1[V + 2], FX[V + 1], FY[V], o[V];
+#pragma unroll
+            for (int y = 0; y < V + 2; ++y) L1[y] = lap_pt(E1[y + 1], E1[y], E1[y + 2], E0[y + 1], E2[y + 1]);
+#pragma unroll
+            for (int y = 0; y < V + 1; ++y) FX[y] = limit(Lj[y + 1] - Lj[y], E0[y + 2] - E0[y + 1]);
+#pragma unroll
+            for (int x = 0; x < V; ++x) FY[x] = limit(L1[x + 1] - Lj[x + 1], E1[x + 2] - E0[x + 2]);
+            const double *cfr = tcf + r * W + lane * V;
+#pragma unroll
+            for (int x = 0; x < V; ++x) o[x] = E0[x + 2] - cfr[x] * ((FX[x + 1] - FX[x]) + (FY[x] - FYm[x]));
+            if (own_valid) {
+                double *op = out_k + j * out.sj + i_own;
+                if (i_own + V <= d.hi[0]) Vec<V>::store(op, o);
+                else {
+#pragma unroll
+                    for (int v = 0; v < V; ++v)
+                        if (i_own + v < d.hi[0]) op[v] = o[v];
+                }
+            }
+#pragma unroll
+            for (int y = 0; y < V + 4; ++y) {
+                E0[y] = E1[y];
+                E1[y] = E2[y];
+            }
+#pragma unroll
+            for (int y = 0; y < V + 2; ++y) Lj[y] = L1[y];
+#pragma unroll
+            for (int x = 0; x < V; ++x) FYm[x] = FY[x];
+        }
+        __syncwarp();
+        if (lane == 0) {
+            const int nxt = item + S * nwt;
+            if (nxt < nitems) {
+                fence_proxy_async();  // our generic-proxy reads of slot s precede the TMA refill
+                issue(nxt, s);
+            }
+        }
+    }
+}
+
+template <int V, int JB, int S, int NW>
+cudaError_t launch_tma(const TMap &tin, const TMap &tcf, const FO &out, const Dom &d, cudaStream_t st, int *launches) {
+    using C = TmaCfg<V, JB, S, NW>;
+    const int ni = d.hi[0] - d.lo[0], nj = d.hi[1] - d.lo[1], nk = d.hi[2] - d.lo[2];
+    const int nseg = (ni + C::W - 1) / C::W, nchunk = (nj + JB - 1) / JB;
+    const long long nitems = (long long)nseg * nchunk * nk;
+    if (nitems > INT32_MAX) return cudaErrorInvalidValue;
+    static bool configured = false;
+    static int blocks_per_sm = 1, sms = 148;
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(hdiff_tma<V, JB, S, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+        if (e != cudaSuccess) return e;
+        int dev;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, hdiff_tma<V, JB, S, NW>, NW * 32, C::SMEM);
+        if (blocks_per_sm < 1) blocks_per_sm = 1;
+        configured = true;
+    }
+    long long blocks = std::min<long long>((nitems + NW - 1) / NW, (long long)sms * blocks_per_sm);
+    hdiff_tma<V, JB, S, NW><<<(unsigned)blocks, NW * 32, C::SMEM, st>>>(tin, tcf, out, d, nseg, nchunk, (int)nitems);
+    ++*launches;
+    return cudaGetLastError();
+}
+
 template <int V, int JB, int P>
 cudaError_t launch_roll(const FV &in, const FV &coeff, const FO &out, const Dom &d, cudaStream_t s, int *launches) {
     constexpr int W = 32 * V;
@@ -273,8 +478,17 @@ cudaError_t launch_roll(const FV &in, const FV &coeff, const FO &out, const Dom 
 
 }  // namespace
 
+void hdiff_tma_boxes(int box_in[3], int box_cf[3]) {
+    box_in[0] = 32 * HD_V + 4;
+    box_in[1] = HD_JB + 4;
+    box_in[2] = 1;
+    box_cf[0] = 32 * HD_V;
+    box_cf[1] = HD_JB;
+    box_cf[2] = 1;
+}
+
 cudaError_t launch_hdiff(const FV &in, const FV &coeff, const FO &out, const Dom &d, int variant, bool aligned16,
-                         cudaStream_t s, int *launches) {
+                         const TMap *tin, const TMap *tcf, cudaStream_t s, int *launches) {
     if (variant == OEC_VARIANT_NAIVE) {
         dim3 block(32, 4, 1);
         dim3 grid((d.hi[0] - d.lo[0] + 31) / 32, (d.hi[1] - d.lo[1] + 3) / 4, d.hi[2] - d.lo[2]);
@@ -282,6 +496,7 @@ cudaError_t launch_hdiff(const FV &in, const FV &coeff, const FO &out, const Dom
         ++*launches;
         return cudaGetLastError();
     }
+    if (tin && tcf && aligned16) return launch_tma<HD_V, HD_JB, HD_S, HD_NW>(*tin, *tcf, out, d, s, launches);
     if (aligned16) return launch_roll<2, 16, 4>(in, coeff, out, d, s, launches);
     return launch_roll<1, 16, 4>(in, coeff, out, d, s, launches);
 }

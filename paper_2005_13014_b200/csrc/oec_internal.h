@@ -4,6 +4,7 @@
 #include <stdint.h>
 
 #include "../../include/oec.h"
+#include "tma.h"
 
 namespace oec {
 
@@ -27,9 +28,11 @@ struct Dom {
 
 // launchers (return cudaGetLastError() of their launches); `launches` is incremented per launch
 cudaError_t launch_hdiff(const FV &in, const FV &coeff, const FO &out, const Dom &d, int variant, bool aligned16,
-                         cudaStream_t s, int *launches);
+                         const TMap *tin, const TMap *tcf, cudaStream_t s, int *launches);
+void hdiff_tma_boxes(int box_in[3], int box_cf[3]);
 cudaError_t launch_vadv(const FV &u_stage, const FV &wcon, const FV &u_pos, const FV &utens, const FV &usi,
-                        const FO &out, double dtr, const Dom &d, cudaStream_t s, int *launches);
+                        const FO &out, double dtr, const Dom &d, const TMap *tmaps, cudaStream_t s, int *launches);
+void vadv_tma_boxes(int K, int box[3], int box_wc[3], bool *fits);
 // suite: inputs / outputs in registry order
 cudaError_t launch_suite(int program_id, const FV *in, const FO *out, const double *scalars, const Dom &d,
                          cudaStream_t s, int *launches);

@@ -317,10 +317,27 @@ static oec_status run_device(int p, const oec_field *const *in, oec_field *const
     int launches = 0;
     cudaError_t e;
     switch (p) {
-    case OEC_PROG_HDIFF: e = launch_hdiff(v_in[0], v_in[1], v_out[0], d, variant, aligned16, s, &launches); break;
-    case OEC_PROG_VADV:
-        e = launch_vadv(v_in[0], v_in[1], v_in[2], v_in[3], v_in[4], v_out[0], sc[0], d, s, &launches);
+    case OEC_PROG_HDIFF: {
+        TMap tin, tcf;
+        int bin[3], bcf[3];
+        hdiff_tma_boxes(bin, bcf);
+        const bool tma = variant == OEC_VARIANT_AUTO && make_tmap(in[0], bin, &tin) && make_tmap(in[1], bcf, &tcf);
+        e = launch_hdiff(v_in[0], v_in[1], v_out[0], d, variant, aligned16, tma ? &tin : nullptr, tma ? &tcf : nullptr,
+                         s, &launches);
         break;
+    }
+    case OEC_PROG_VADV: {
+        // TMA path: u_stage, wcon, u_pos, utens, utens_stage_in (tmaps[0..4])
+        TMap tm[5];
+        int box[3], bwc[3];
+        bool fits;
+        vadv_tma_boxes((int)(hi[2] - lo[2]), box, bwc, &fits);
+        bool tma = fits && aligned16 && variant == OEC_VARIANT_AUTO;
+        for (int q = 0; q < 5 && tma; ++q) tma = make_tmap(in[q], q == 1 ? bwc : box, &tm[q]);
+        e = launch_vadv(v_in[0], v_in[1], v_in[2], v_in[3], v_in[4], v_out[0], sc[0], d, tma ? tm : nullptr, s,
+                        &launches);
+        break;
+    }
     default: e = launch_suite(p, v_in, v_out, sc, d, s, &launches); break;
     }
     if (e != cudaSuccess) return set_error(OEC_ERR_CUDA, "%s: kernel launch failed: %s", P.name, cudaGetErrorString(e));

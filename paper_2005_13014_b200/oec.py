@@ -17,7 +17,7 @@ from typing import Dict, List, Optional, Sequence, Tuple
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "liboec.so")
+LIB_PATH = os.environ.get("OEC_LIB_PATH") or os.path.join(_HERE, "liboec.so")
 
 OEC_OK = 0
 OEC_DEVICE_HOST = -1
