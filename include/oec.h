@@ -228,6 +228,16 @@ oec_status oec_halo_exchange_local(const int64_t global_domain[3], int32_t px, i
 
 oec_status oec_decomp_destroy(oec_decomp *d);
 
+/* ----------------------------------------------------------------------------------------- */
+/* Self-test (used by the GPU test suite).                                                    */
+/* ----------------------------------------------------------------------------------------- */
+/* The vadv kernel computes the fp64 reciprocal with the branch-free instruction sequence of the
+ * CUDA IEEE fast path and falls back to 1.0/x where that path does not apply.  This runs it on n
+ * pseudo-random doubles (seeded) on the current device and reports how many it checked (fast
+ * path applicable) and how many differed bitwise from 1.0/x (must be 0).  Synchronous. */
+oec_status oec_selftest_rcp(unsigned long long n, unsigned long long seed, unsigned long long *mismatches,
+                            unsigned long long *checked);
+
 #ifdef __cplusplus
 }
 #endif

@@ -95,7 +95,7 @@ struct Vec<2> {
 };
 
 template <>
-struct Vec<4> {
+struct __attribute__((unused)) Vec<4> {
     static __device__ __forceinline__ void load(const double *p, double *v) {
         Vec<2>::load(p, v);
         Vec<2>::load(p + 2, v + 2);
@@ -327,6 +327,62 @@ __device__ __forceinline__ void lds_row(const double *row, int lane, double *e) 
     }
 }
 
+// One W x JB tile from shared memory: rows 0..JB+3 of `tin` are j0-2 .. j0+JB+1 (each W+4 wide,
+// element x <-> i = ib-2+x), `tcf` holds coeff rows j0 .. j0+JB-1 (W wide).  FULL: all JB rows are
+// in the domain -> the row loop is fully unrolled without checks (registers renamed, no moves).
+template <int V, int JB, bool FULL>
+__device__ __forceinline__ void hdiff_tile(const double *tin, const double *tcf, double *out_k, int sj, int j0,
+                                           int nrows, int i_own, int hi0, int lane) {
+    constexpr int W = 32 * V;
+    const bool own_valid = i_own < hi0;
+    const bool own_full = i_own + V <= hi0;
+    double E0[V + 4], E1[V + 4], E2[V + 4], Lj[V + 2], FYm[V];
+    {
+        double Em2[V + 4], Em1[V + 4], Lm[V];
+        lds_row<V>(tin + 0 * (W + 4), lane, Em2);
+        lds_row<V>(tin + 1 * (W + 4), lane, Em1);
+        lds_row<V>(tin + 2 * (W + 4), lane, E0);
+        lds_row<V>(tin + 3 * (W + 4), lane, E1);
+#pragma unroll
+        for (int x = 0; x < V; ++x) Lm[x] = lap_pt(Em1[x + 2], Em1[x + 1], Em1[x + 3], Em2[x + 2], E0[x + 2]);
+#pragma unroll
+        for (int y = 0; y < V + 2; ++y) Lj[y] = lap_pt(E0[y + 1], E0[y], E0[y + 2], Em1[y + 1], E1[y + 1]);
+#pragma unroll
+        for (int x = 0; x < V; ++x) FYm[x] = limit(Lj[x + 1] - Lm[x], E0[x + 2] - Em1[x + 2]);
+    }
+#pragma unroll
+    for (int r = 0; r < JB; ++r) {
+        if (!FULL && r >= nrows) break;  // warp-uniform
+        lds_row<V>(tin + (r + 4) * (W + 4), lane, E2);
+        double L1[V + 2], FX[V + 1], FY[V], o[V];
+#pragma unroll
+        for (int y = 0; y < V + 2; ++y) L1[y] = lap_pt(E1[y + 1], E1[y], E1[y + 2], E0[y + 1], E2[y + 1]);
+#pragma unroll
+        for (int y = 0; y < V + 1; ++y) FX[y] = limit(Lj[y + 1] - Lj[y], E0[y + 2] - E0[y + 1]);
+#pragma unroll
+        for (int x = 0; x < V; ++x) FY[x] = limit(L1[x + 1] - Lj[x + 1], E1[x + 2] - E0[x + 2]);
+        const double *cfr = tcf + r * W + lane * V;
+#pragma unroll
+        for (int x = 0; x < V; ++x) o[x] = E0[x + 2] - cfr[x] * ((FX[x + 1] - FX[x]) + (FY[x] - FYm[x]));
+        double *op = out_k + (j0 + r) * sj + i_own;
+        if (own_full) Vec<V>::store(op, o);
+        else if (own_valid) {
+#pragma unroll
+            for (int v = 0; v < V; ++v)
+                if (i_own + v < hi0) op[v] = o[v];
+        }
+#pragma unroll
+        for (int y = 0; y < V + 4; ++y) {
+            E0[y] = E1[y];
+            E1[y] = E2[y];
+        }
+#pragma unroll
+        for (int y = 0; y < V + 2; ++y) Lj[y] = L1[y];
+#pragma unroll
+        for (int x = 0; x < V; ++x) FYm[x] = FY[x];
+    }
+}
+
 template <int V, int JB, int S, int NW>
 __global__ void __launch_bounds__(NW * 32, 1) hdiff_tma(const __grid_constant__ TMap m_in, const __grid_constant__ TMap m_cf,
                                                      FO out, Dom d, int nseg, int nchunk, int nitems) {
@@ -369,64 +425,16 @@ __global__ void __launch_bounds__(NW * 32, 1) hdiff_tma(const __grid_constant__ 
     int n = 0;
     for (int item = gw; item < nitems; item += nwt, ++n) {
         const int s = n % S;
-        mbar_wait(&bars[s], (n / S) & 1);
         int ib, j0, k;
         decode(item, ib, j0, k);
-        const int j1 = min(j0 + JB, d.hi[1]);
+        const int nrows = min(JB, d.hi[1] - j0);
         const int i_own = ib + lane * V;
-        const bool own_valid = i_own < d.hi[0];
-        const double *tin = in_s(s);
-        const double *tcf = cf_s(s);
         double *out_k = out.p + k * out.sk;
-
-        double E0[V + 4], E1[V + 4], E2[V + 4], Lj[V + 2], FYm[V];
-        {
-            double Em2[V + 4], Em1[V + 4], Lm[V];
-            lds_row<V>(tin + 0 * (W + 4), lane, Em2);
-            lds_row<V>(tin + 1 * (W + 4), lane, Em1);
-            lds_row<V>(tin + 2 * (W + 4), lane, E0);
-            lds_row<V>(tin + 3 * (W + 4), lane, E1);
-#pragma unroll
-            for (int x = 0; x < V; ++x) Lm[x] = lap_pt(Em1[x + 2], Em1[x + 1], Em1[x + 3], Em2[x + 2], E0[x + 2]);
-#pragma unroll
-            for (int y = 0; y < V + 2; ++y) Lj[y] = lap_pt(E0[y + 1], E0[y], E0[y + 2], Em1[y + 1], E1[y + 1]);
-#pragma unroll
-            for (int x = 0; x < V; ++x) FYm[x] = limit(Lj[x + 1] - Lm[x], E0[x + 2] - Em1[x + 2]);
-        }
-#pragma unroll 2
-        for (int r = 0; r < JB; ++r) {
-            const int j = j0 + r;
-            if (j >= j1) break;  // warp-uniform
-            lds_row<V>(tin + (r + 4) * (W + 4), lane, E2);
-            double L1[V + 2], FX[V + 1], FY[V], o[V];
-#pragma unroll
-            for (int y = 0; y < V + 2; ++y) L1[y] = lap_pt(E1[y + 1], E1[y], E1[y + 2], E0[y + 1], E2[y + 1]);
-#pragma unroll
-            for (int y = 0; y < V + 1; ++y) FX[y] = limit(Lj[y + 1] - Lj[y], E0[y + 2] - E0[y + 1]);
-#pragma unroll
-            for (int x = 0; x < V; ++x) FY[x] = limit(L1[x + 1] - Lj[x + 1], E1[x + 2] - E0[x + 2]);
-            const double *cfr = tcf + r * W + lane * V;
-#pragma unroll
-            for (int x = 0; x < V; ++x) o[x] = E0[x + 2] - cfr[x] * ((FX[x + 1] - FX[x]) + (FY[x] - FYm[x]));
-            if (own_valid) {
-                double *op = out_k + j * out.sj + i_own;
-                if (i_own + V <= d.hi[0]) Vec<V>::store(op, o);
-                else {
-#pragma unroll
-                    for (int v = 0; v < V; ++v)
-                        if (i_own + v < d.hi[0]) op[v] = o[v];
-                }
-            }
-#pragma unroll
-            for (int y = 0; y < V + 4; ++y) {
-                E0[y] = E1[y];
-                E1[y] = E2[y];
-            }
-#pragma unroll
-            for (int y = 0; y < V + 2; ++y) Lj[y] = L1[y];
-#pragma unroll
-            for (int x = 0; x < V; ++x) FYm[x] = FY[x];
-        }
+        mbar_wait(&bars[s], (n / S) & 1);
+        if (nrows == JB)
+            hdiff_tile<V, JB, true>(in_s(s), cf_s(s), out_k, out.sj, j0, JB, i_own, d.hi[0], lane);
+        else
+            hdiff_tile<V, JB, false>(in_s(s), cf_s(s), out_k, out.sj, j0, nrows, i_own, d.hi[0], lane);
         __syncwarp();
         if (lane == 0) {
             const int nxt = item + S * nwt;

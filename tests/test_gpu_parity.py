@@ -177,11 +177,11 @@ def test_torch_wrapped_fields():
 
     from paper_2005_13014_b200 import oec
 
-    domain = (50, 30, 7)
+    domain = (51, 30, 7)  # odd pitch: no 16-byte alignment -> the non-TMA register kernel
     host = synth.make_inputs("hdiff", domain, seed=7)
     t_in = torch.from_numpy(host["in"].data).cuda()
     t_cf = torch.from_numpy(host["coeff"].data).cuda()
-    t_out = torch.full((7, 30, 50), float("nan"), dtype=torch.float64, device="cuda")
+    t_out = torch.full((7, 30, 51), float("nan"), dtype=torch.float64, device="cuda")
     oec.oec_hdiff(oec.oec_field_wrap(t_in, host["in"].lb, host["in"].ub),
                   oec.oec_field_wrap(t_cf, (0, 0, 0), domain), oec.oec_field_wrap(t_out, (0, 0, 0), domain),
                   (0, 0, 0), domain)
@@ -201,3 +201,36 @@ def test_full_size_sampled(program):
     for lo, hi in [((0, 0, 0), (64, 48, 80)), ((960, 976, 0), (1024, 1024, 80)), ((500, 300, 0), (580, 340, 80))]:
         r = run_oracle(program, host, domain, dom_lb=lo, dom_ub=hi)
         _assert_parity(domain_part(g[name], lo, hi), r[name], (program, lo, hi))
+
+
+def test_branch_free_reciprocal_is_ieee():
+    # vadv's chain uses the CUDA IEEE reciprocal fast path without its branch (DESIGN.md "vadv
+    # kernel"); wherever that path applies it must equal 1.0/x bit for bit
+    from paper_2005_13014_b200 import oec
+
+    bad, used = oec.oec_selftest_rcp(200_000_000, seed=12345)
+    assert used > 150_000_000 and bad == 0, (bad, used)
+
+
+@pytest.mark.parametrize("K", [84, 85, 100, 128, 129, 200, 260])
+def test_vadv_tall_columns_every_kernel(K):
+    # K <= 84: vadv_ws2 (c', d', u_pos in TMEM); <= 128: vadv_ws (c', d' in TMEM); <= ~190: vadv_tma
+    # (c', d' in shared memory); taller: the register kernel with a global c'/d' workspace
+    _check("vadv", (130, 3, K), seed=K)
+
+
+def test_vadv_odd_pitch_register_kernel():
+    # torch-wrapped fields with odd strides cannot be TMA tensors: the register-prefetch kernel runs
+    import torch
+
+    from paper_2005_13014_b200 import oec
+
+    domain = (45, 7, 9)
+    host = synth.make_inputs("vadv", domain, seed=8)
+    ins = [oec.oec_field_wrap(torch.from_numpy(host[s.name].data).cuda(), host[s.name].lb, host[s.name].ub)
+           for s in synth.PROGRAMS["vadv"].inputs]
+    t_out = torch.full((9, 7, 45), float("nan"), dtype=torch.float64, device="cuda")
+    oec.oec_vadv(*ins, oec.oec_field_wrap(t_out, (0, 0, 0), domain), 0.15, (0, 0, 0), domain)
+    torch.cuda.synchronize()
+    r = run_oracle("vadv", host, domain)
+    _assert_parity(t_out.cpu().numpy(), r["utens_stage_out"], "vadv odd pitch")

@@ -1,0 +1,13 @@
+#!/bin/bash
+cd "$GRAFT_REPO_ROOT" || exit 1
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu3.txt 2>&1; echo "pytest exit $?" >> gpurun_out/pytest_gpu3.txt
+: > gpurun_out/tune3.jsonl
+python tools/kernel_bench.py --programs hdiff vadv --tag default >> gpurun_out/tune3.jsonl 2>&1
+for f in tune/*.so; do OEC_LIB_PATH=$f timeout 120 python tools/kernel_bench.py --programs hdiff vadv --tag $(basename $f .so) >> gpurun_out/tune3.jsonl 2>&1; done
+python tools/kernel_bench.py --programs hdiff vadv --domain 1024 1024 80 --reps 5 --tag big >> gpurun_out/tune3.jsonl 2>&1
+python tools/kernel_bench.py --programs hdiff vadv --domain 256 256 60 --tag paper_large >> gpurun_out/tune3.jsonl 2>&1
+for p in hdiff vadv; do
+  timeout 300 ncu --set full --clock-control none --import-source on -k regex:"${p}_t" -s 2 -c 1 -o gpurun_out/prof3_${p} -f python tools/kernel_driver.py --program $p --reps 4 > gpurun_out/ncu3_${p}.log 2>&1
+done
+echo done

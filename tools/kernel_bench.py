@@ -32,6 +32,26 @@ def main():
     l2 = torch.cuda.get_device_properties(0).L2_cache_size
     peak, _ = hbm_peak()
     for program in a.programs:
+        if program == "copy":  # practical roofline at this size: torch copy_ of a 16 MiB buffer (32 MiB traffic)
+            n = 2 * 2**20
+            bufs = [(torch.rand(n, dtype=torch.float64, device="cuda"), torch.empty(n, dtype=torch.float64, device="cuda"))
+                    for _ in range(12)]
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                for x, y in bufs:
+                    y.copy_(x)
+            g.replay()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(a.reps):
+                g.replay()
+            e1.record()
+            torch.cuda.synchronize()
+            us = 1e3 * e0.elapsed_time(e1) / (a.reps * len(bufs))
+            print(json.dumps({"tag": a.tag, "program": "copy16MiB", "us": round(us, 3),
+                              "GB/s": round(2 * n * 8 / (us * 1e-6) / 1e9, 1)}), flush=True)
+            continue
         host = synth.make_inputs(program, dom, seed=0)
         spec = synth.PROGRAMS[program]
         sc = [v for _, v in spec.scalars]
