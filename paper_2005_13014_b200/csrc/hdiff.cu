@@ -336,6 +336,7 @@ __device__ __forceinline__ void hdiff_tile(const double *tin, const double *tcf,
     constexpr int W = 32 * V;
     const bool own_valid = i_own < hi0;
     const bool own_full = i_own + V <= hi0;
+    const bool warp_full = __all_sync(0xffffffffu, own_full);
     double E0[V + 4], E1[V + 4], E2[V + 4], Lj[V + 2], FYm[V];
     {
         double Em2[V + 4], Em1[V + 4], Lm[V];
@@ -365,7 +366,8 @@ __device__ __forceinline__ void hdiff_tile(const double *tin, const double *tcf,
 #pragma unroll
         for (int x = 0; x < V; ++x) o[x] = E0[x + 2] - cfr[x] * ((FX[x + 1] - FX[x]) + (FY[x] - FYm[x]));
         double *op = out_k + (j0 + r) * sj + i_own;
-        if (own_full) Vec<V>::store(op, o);
+        if (warp_full) Vec<V>::store(op, o);  // warp-uniform: no per-lane branch
+        else if (own_full) Vec<V>::store(op, o);
         else if (own_valid) {
 #pragma unroll
             for (int v = 0; v < V; ++v)

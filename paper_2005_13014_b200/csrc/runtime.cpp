@@ -329,11 +329,11 @@ static oec_status run_device(int p, const oec_field *const *in, oec_field *const
     case OEC_PROG_VADV: {
         // TMA path: u_stage, wcon, u_pos, utens, utens_stage_in (tmaps[0..4])
         TMap tm[5];
-        int box[3], bwc[3];
+        int box[3], bwc[3], bus[3];
         bool fits;
-        vadv_tma_boxes(d, box, bwc, &fits);
+        vadv_tma_boxes(d, box, bwc, bus, &fits);
         bool tma = fits && aligned16 && variant == OEC_VARIANT_AUTO;
-        for (int q = 0; q < 5 && tma; ++q) tma = make_tmap(in[q], q == 1 ? bwc : box, &tm[q]);
+        for (int q = 0; q < 5 && tma; ++q) tma = make_tmap(in[q], q == 0 ? bus : (q == 1 ? bwc : box), &tm[q]);
         e = launch_vadv(v_in[0], v_in[1], v_in[2], v_in[3], v_in[4], v_out[0], sc[0], d, tma ? tm : nullptr, s,
                         &launches);
         break;

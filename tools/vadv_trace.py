@@ -28,7 +28,7 @@ def main():
     oec.lib().oec_debug_vadv_trace(buf)
     t = np.array(buf[:], dtype=np.int64).reshape(8, 256)
     t0 = t[7, 0]
-    names = ["producer issued", "coef got input", "coef got row slot", "chain got rows", "chain stored tmem",
+    names = ["producer issued", "coef got input", "sp: coef0|coef1|chain0..", "chain got rows", "chain stored tmem",
              "coef rows written", "chain done", "start"]
     print("end-to-end CTA(0,0) us:", (t[6, 0] - t0) / 1e3)
     for role in range(6):
