@@ -14,19 +14,20 @@ struct Pt {
 };
 
 __device__ __forceinline__ double A(const FV &f, int i, int j, int k) { return __ldg(f.p + (i + j * f.sj + k * f.sk)); }
-__device__ __forceinline__ void S(const FO &f, int i, int j, int k, double v) { f.p[i + j * f.sj + k * f.sk] = v; }
+// point functions return their outputs in r[]; the kernel stores them after all loads of its levels
+#define OUT(o, v) (r[o] = (v))
 
 // ---------------------------------------------------------------------------------------------
 // uvbke:  ub = (dt5 ((uc[j-1] + uc) - (vc[i-1] + vc) cosa)) rsina ;  vb analogous
 // ---------------------------------------------------------------------------------------------
-__device__ void uvbke_pt(const FV *in, const FO *out, const double *sc, int i, int j, int k) {
+__device__ __forceinline__ void uvbke_pt(const FV *in, const double *sc, int i, int j, int k, double *r) {
     const FV &uc = in[0], &vc = in[1], &cosa = in[2], &rsina = in[3];
     const double dt5 = sc[0];
     const double u2 = A(uc, i, j - 1, k) + A(uc, i, j, k);
     const double v2 = A(vc, i - 1, j, k) + A(vc, i, j, k);
     const double ca = A(cosa, i, j, k), rs = A(rsina, i, j, k);
-    S(out[0], i, j, k, (dt5 * (u2 - v2 * ca)) * rs);
-    S(out[1], i, j, k, (dt5 * (v2 - u2 * ca)) * rs);
+    OUT(0, (dt5 * (u2 - v2 * ca)) * rs);
+    OUT(1, (dt5 * (v2 - u2 * ca)) * rs);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -34,7 +35,7 @@ __device__ void uvbke_pt(const FV *in, const FO *out, const double *sc, int i, i
 //   uc' = uc + ((dt2 rdxc) / (wk[i-1] + wk)) * ((gz[i-1,k+1] - gz)(pkc[k+1] - pkc[i-1])
 //                                                + (gz[i-1] - gz[k+1])(pkc[i-1,k+1] - pkc))
 // ---------------------------------------------------------------------------------------------
-__device__ void p_grad_c_pt(const FV *in, const FO *out, const double *sc, int i, int j, int k) {
+__device__ __forceinline__ void p_grad_c_pt(const FV *in, const double *sc, int i, int j, int k, double *r) {
     const FV &uc = in[0], &vc = in[1], &delpc = in[2], &pkc = in[3], &gz = in[4], &rdxc = in[5], &rdyc = in[6];
     const double dt2 = sc[0];
     const double gz0 = A(gz, i, j, k), gz1 = A(gz, i, j, k + 1), pk0 = A(pkc, i, j, k), pk1 = A(pkc, i, j, k + 1);
@@ -42,12 +43,12 @@ __device__ void p_grad_c_pt(const FV *in, const FO *out, const double *sc, int i
     {
         const double t = (A(gz, i - 1, j, k + 1) - gz0) * (pk1 - A(pkc, i - 1, j, k)) +
                          (A(gz, i - 1, j, k) - gz1) * (A(pkc, i - 1, j, k + 1) - pk0);
-        S(out[0], i, j, k, A(uc, i, j, k) + ((dt2 * A(rdxc, i, j, k)) / (A(delpc, i - 1, j, k) + wk)) * t);
+        OUT(0, A(uc, i, j, k) + ((dt2 * A(rdxc, i, j, k)) / (A(delpc, i - 1, j, k) + wk)) * t);
     }
     {
         const double t = (A(gz, i, j - 1, k + 1) - gz0) * (pk1 - A(pkc, i, j - 1, k)) +
                          (A(gz, i, j - 1, k) - gz1) * (A(pkc, i, j - 1, k + 1) - pk0);
-        S(out[1], i, j, k, A(vc, i, j, k) + ((dt2 * A(rdyc, i, j, k)) / (A(delpc, i, j - 1, k) + wk)) * t);
+        OUT(1, A(vc, i, j, k) + ((dt2 * A(rdyc, i, j, k)) / (A(delpc, i, j - 1, k) + wk)) * t);
     }
 }
 
@@ -57,7 +58,7 @@ __device__ void p_grad_c_pt(const FV *in, const FO *out, const double *sc, int i
 //   u' = ((u + du) + (dt / (delp + delp[i+1])) ((gz[k+1] - gz[i+1])(pp[i+1,k+1] - pp)
 //                                                + (gz - gz[i+1,k+1])(pp[k+1] - pp[i+1]))) rdx
 // ---------------------------------------------------------------------------------------------
-__device__ void nh_p_grad_pt(const FV *in, const FO *out, const double *sc, int i, int j, int k) {
+__device__ __forceinline__ void nh_p_grad_pt(const FV *in, const double *sc, int i, int j, int k, double *r) {
     const FV &u = in[0], &v = in[1], &pp = in[2], &gz = in[3], &pk3 = in[4], &delp = in[5], &rdx = in[6], &rdy = in[7];
     const double dt = sc[0];
     const double gz0 = A(gz, i, j, k), gz1 = A(gz, i, j, k + 1);
@@ -72,7 +73,7 @@ __device__ void nh_p_grad_pt(const FV *in, const FO *out, const double *sc, int 
         const double du = (dt / (wk + wkE)) * ((gz1 - gzE) * (pkE1 - pk0) + (gz0 - gzE1) * (pk1 - pkE));
         const double nh = (dt / (dl + A(delp, i + 1, j, k))) *
                           ((gz1 - gzE) * (A(pp, i + 1, j, k + 1) - pp0) + (gz0 - gzE1) * (pp1 - A(pp, i + 1, j, k)));
-        S(out[0], i, j, k, ((A(u, i, j, k) + du) + nh) * A(rdx, i, j, k));
+        OUT(0, ((A(u, i, j, k) + du) + nh) * A(rdx, i, j, k));
     }
     {  // j direction
         const double gzN = A(gz, i, j + 1, k), gzN1 = A(gz, i, j + 1, k + 1);
@@ -81,7 +82,7 @@ __device__ void nh_p_grad_pt(const FV *in, const FO *out, const double *sc, int 
         const double dv = (dt / (wk + wkN)) * ((gz1 - gzN) * (pkN1 - pk0) + (gz0 - gzN1) * (pk1 - pkN));
         const double nh = (dt / (dl + A(delp, i, j + 1, k))) *
                           ((gz1 - gzN) * (A(pp, i, j + 1, k + 1) - pp0) + (gz0 - gzN1) * (pp1 - A(pp, i, j + 1, k)));
-        S(out[1], i, j, k, ((A(v, i, j, k) + dv) + nh) * A(rdy, i, j, k));
+        OUT(1, ((A(v, i, j, k) + dv) + nh) * A(rdy, i, j, k));
     }
 }
 
@@ -111,34 +112,34 @@ __device__ __forceinline__ double ppm_flux(const FV &q, double c, int i, int j, 
 }
 
 // fvtp2d_qi: fy2 = flux_y(q, cry); fyy = yfx fy2; q_i = ((q area + fyy) - fyy[j+1]) / ra_y
-__device__ void fvtp2d_qi_pt(const FV *in, const FO *out, const double *, int i, int j, int k) {
+__device__ __forceinline__ void fvtp2d_qi_pt(const FV *in, const double *, int i, int j, int k, double *r) {
     const FV &q = in[0], &cry = in[1], &yfx = in[2], &area = in[3], &ra_y = in[4];
     const double fy2 = ppm_flux(q, A(cry, i, j, k), i, j, k, 0, 1);
     const double fy2n = ppm_flux(q, A(cry, i, j + 1, k), i, j + 1, k, 0, 1);
     const double fyy = A(yfx, i, j, k) * fy2, fyyn = A(yfx, i, j + 1, k) * fy2n;
-    S(out[0], i, j, k, ((A(q, i, j, k) * A(area, i, j, k) + fyy) - fyyn) / A(ra_y, i, j, k));
-    S(out[1], i, j, k, fy2);
+    OUT(0, ((A(q, i, j, k) * A(area, i, j, k) + fyy) - fyyn) / A(ra_y, i, j, k));
+    OUT(1, fy2);
 }
 
 // fvtp2d_qj: fx = flux_x(q_i, crx); fx2 = flux_x(q, crx); fx1 = xfx fx2; q_j = ((q area + fx1) - fx1[i+1]) / ra_x
-__device__ void fvtp2d_qj_pt(const FV *in, const FO *out, const double *, int i, int j, int k) {
+__device__ __forceinline__ void fvtp2d_qj_pt(const FV *in, const double *, int i, int j, int k, double *r) {
     const FV &q = in[0], &q_i = in[1], &crx = in[2], &xfx = in[3], &area = in[4], &ra_x = in[5];
     const double c0 = A(crx, i, j, k), c1 = A(crx, i + 1, j, k);
     const double fx = ppm_flux(q_i, c0, i, j, k, 1, 0);
     const double fx2 = ppm_flux(q, c0, i, j, k, 1, 0);
     const double fx2n = ppm_flux(q, c1, i + 1, j, k, 1, 0);
     const double fx1 = A(xfx, i, j, k) * fx2, fx1n = A(xfx, i + 1, j, k) * fx2n;
-    S(out[0], i, j, k, ((A(q, i, j, k) * A(area, i, j, k) + fx1) - fx1n) / A(ra_x, i, j, k));
-    S(out[1], i, j, k, fx);
-    S(out[2], i, j, k, fx2);
+    OUT(0, ((A(q, i, j, k) * A(area, i, j, k) + fx1) - fx1n) / A(ra_x, i, j, k));
+    OUT(1, fx);
+    OUT(2, fx2);
 }
 
 // fvtp2d_flux: fy = flux_y(q_j, cry); fx_out = (0.5 (fx + fx2)) mfx; fy_out = (0.5 (fy + fy2)) mfy
-__device__ void fvtp2d_flux_pt(const FV *in, const FO *out, const double *, int i, int j, int k) {
+__device__ __forceinline__ void fvtp2d_flux_pt(const FV *in, const double *, int i, int j, int k, double *r) {
     const FV &q_j = in[0], &cry = in[1], &fx = in[2], &fx2 = in[3], &fy2 = in[4], &mfx = in[5], &mfy = in[6];
     const double fy = ppm_flux(q_j, A(cry, i, j, k), i, j, k, 0, 1);
-    S(out[0], i, j, k, (0.5 * (A(fx, i, j, k) + A(fx2, i, j, k))) * A(mfx, i, j, k));
-    S(out[1], i, j, k, (0.5 * (fy + A(fy2, i, j, k))) * A(mfy, i, j, k));
+    OUT(0, (0.5 * (A(fx, i, j, k) + A(fx2, i, j, k))) * A(mfx, i, j, k));
+    OUT(1, (0.5 * (fy + A(fy2, i, j, k))) * A(mfy, i, j, k));
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -156,7 +157,7 @@ __device__ __forceinline__ double fw_ppgc(const FV &ppuv, const FV &wgt, int i, 
     return g1 - g0;
 }
 
-__device__ void fastwaves_pt(const FV *in, const FO *out, const double *sc, int i, int j, int k) {
+__device__ __forceinline__ void fastwaves_pt(const FV *in, const double *sc, int i, int j, int k, double *r) {
     const FV &u_pos = in[0], &v_pos = in[1], &u_tens = in[2], &v_tens = in[3], &rho = in[4], &ppuv = in[5], &fx = in[6],
              &wgt = in[7], &hhl = in[8];
     const double edadlat = sc[0], dt = sc[1];
@@ -167,7 +168,7 @@ __device__ void fastwaves_pt(const FV *in, const FO *out, const double *sc, int 
         const double ppgu = (A(ppuv, i + 1, j, k) - p0) +
                             (((fw_ppgc(ppuv, wgt, i + 1, j, k) + pc) * 0.5) * ((h1 + h0) - (hE1 + hE))) /
                                 ((h1 - h0) + (hE1 - hE));
-        S(out[0], i, j, k,
+        OUT(0,
           A(u_pos, i, j, k) + (A(u_tens, i, j, k) - ((ppgu * 2.0) * A(fx, i, j, k)) / (A(rho, i + 1, j, k) + r0)) * dt);
     }
     {
@@ -175,7 +176,7 @@ __device__ void fastwaves_pt(const FV *in, const FO *out, const double *sc, int 
         const double ppgv = (A(ppuv, i, j + 1, k) - p0) +
                             (((fw_ppgc(ppuv, wgt, i, j + 1, k) + pc) * 0.5) * ((h1 + h0) - (hN1 + hN))) /
                                 ((h1 - h0) + (hN1 - hN));
-        S(out[1], i, j, k,
+        OUT(1,
           A(v_pos, i, j, k) + (A(v_tens, i, j, k) - ((ppgv * 2.0) * edadlat) / (A(rho, i, j + 1, k) + r0)) * dt);
     }
 }
@@ -187,15 +188,36 @@ struct SuiteArgs {
     double sc[2];
     Dom d;
 };
-typedef void (*PointFn)(const FV *, const FO *, const double *, int, int, int);
+typedef void (*PointFn)(const FV *, const double *, int, int, int, double *);
 
-template <PointFn F>
-__global__ void __launch_bounds__(128) suite_kernel(const __grid_constant__ SuiteArgs a) {
-    const int i = a.d.lo[0] + blockIdx.x * 32 + threadIdx.x;
-    const int j = a.d.lo[1] + blockIdx.y * 4 + threadIdx.y;
-    const int k = a.d.lo[2] + blockIdx.z;
+#ifndef SU_BX
+#define SU_BX 32
+#endif
+#ifndef SU_BY
+#define SU_BY 4
+#endif
+#ifndef SU_KC
+#define SU_KC 1
+#endif
+
+// One thread computes KC consecutive levels of one (i, j): every load of the KC levels is issued
+// before any store (outputs are kept in registers), so the loads overlap (memory-level
+// parallelism) and loads shared between levels (k+1 of level k = k of level k+1) are reused.
+template <PointFn F, int NO, int KC>
+__global__ void __launch_bounds__(SU_BX * SU_BY) suite_kernel(const __grid_constant__ SuiteArgs a) {
+    const int i = a.d.lo[0] + blockIdx.x * SU_BX + threadIdx.x;
+    const int j = a.d.lo[1] + blockIdx.y * SU_BY + threadIdx.y;
+    const int k0 = a.d.lo[2] + blockIdx.z * KC;
     if (i >= a.d.hi[0] || j >= a.d.hi[1]) return;
-    F(a.in, a.out, a.sc, i, j, k);
+    double r[KC][NO];
+#pragma unroll
+    for (int kk = 0; kk < KC; ++kk) F(a.in, a.sc, i, j, min(k0 + kk, a.d.hi[2] - 1), r[kk]);
+#pragma unroll
+    for (int kk = 0; kk < KC; ++kk)
+        if (k0 + kk < a.d.hi[2]) {
+#pragma unroll
+            for (int o = 0; o < NO; ++o) a.out[o].p[i + j * a.out[o].sj + (k0 + kk) * a.out[o].sk] = r[kk][o];
+        }
 }
 
 }  // namespace
@@ -208,16 +230,18 @@ cudaError_t launch_suite(int program_id, const FV *in, const FO *out, const doub
     a.sc[0] = scalars[0];
     a.sc[1] = scalars[1];
     a.d = d;
-    dim3 block(32, 4, 1);
-    dim3 grid((d.hi[0] - d.lo[0] + 31) / 32, (d.hi[1] - d.lo[1] + 3) / 4, d.hi[2] - d.lo[2]);
+    constexpr int KC = SU_KC;
+    dim3 block(SU_BX, SU_BY, 1);
+    dim3 grid((d.hi[0] - d.lo[0] + SU_BX - 1) / SU_BX, (d.hi[1] - d.lo[1] + SU_BY - 1) / SU_BY,
+              (d.hi[2] - d.lo[2] + KC - 1) / KC);
     switch (program_id) {
-    case OEC_PROG_UVBKE: suite_kernel<uvbke_pt><<<grid, block, 0, s>>>(a); break;
-    case OEC_PROG_P_GRAD_C: suite_kernel<p_grad_c_pt><<<grid, block, 0, s>>>(a); break;
-    case OEC_PROG_NH_P_GRAD: suite_kernel<nh_p_grad_pt><<<grid, block, 0, s>>>(a); break;
-    case OEC_PROG_FVTP2D_QI: suite_kernel<fvtp2d_qi_pt><<<grid, block, 0, s>>>(a); break;
-    case OEC_PROG_FVTP2D_QJ: suite_kernel<fvtp2d_qj_pt><<<grid, block, 0, s>>>(a); break;
-    case OEC_PROG_FVTP2D_FLUX: suite_kernel<fvtp2d_flux_pt><<<grid, block, 0, s>>>(a); break;
-    case OEC_PROG_FASTWAVES: suite_kernel<fastwaves_pt><<<grid, block, 0, s>>>(a); break;
+    case OEC_PROG_UVBKE: suite_kernel<uvbke_pt, 2, KC><<<grid, block, 0, s>>>(a); break;
+    case OEC_PROG_P_GRAD_C: suite_kernel<p_grad_c_pt, 2, KC><<<grid, block, 0, s>>>(a); break;
+    case OEC_PROG_NH_P_GRAD: suite_kernel<nh_p_grad_pt, 2, KC><<<grid, block, 0, s>>>(a); break;
+    case OEC_PROG_FVTP2D_QI: suite_kernel<fvtp2d_qi_pt, 2, KC><<<grid, block, 0, s>>>(a); break;
+    case OEC_PROG_FVTP2D_QJ: suite_kernel<fvtp2d_qj_pt, 3, KC><<<grid, block, 0, s>>>(a); break;
+    case OEC_PROG_FVTP2D_FLUX: suite_kernel<fvtp2d_flux_pt, 2, KC><<<grid, block, 0, s>>>(a); break;
+    case OEC_PROG_FASTWAVES: suite_kernel<fastwaves_pt, 2, KC><<<grid, block, 0, s>>>(a); break;
     default: return cudaErrorInvalidValue;
     }
     ++*launches;
