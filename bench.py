@@ -407,9 +407,10 @@ def main():
         e2e = e2e_measure(oec, torch, hh, vh, dtr, domain, args.e2e_steps, world)
 
     # ---- remaining suite (evidence for SURVEY §8(a) a7; not part of the step) ----
-    suite_res = None
+    suite_res = levels = None
     if not args.no_suite and world == 1:
         suite_res = suite_measure(oec, torch, domain, l2, peak)
+        levels = levels_measure(oec, torch, domain, l2, peak)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -437,6 +438,8 @@ def main():
         }
         if suite_res is not None:
             res["suite"] = suite_res
+        if levels is not None:
+            res["optimization_levels"] = levels
         print(json.dumps(res), flush=True)
     if world > 1:
         dist.barrier()
@@ -481,43 +484,60 @@ def e2e_measure(oec, torch, hh, vh, dtr, domain, steps, world):
             "path": "oec_hdiff/oec_vadv with OEC_DEVICE_HOST fields (pinned), staged by liboec, synchronous"}
 
 
-def suite_measure(oec, torch, domain, l2, peak, reps=20):
-    res = {}
-    for program in synth.SUITE:
-        host = synth.make_inputs(program, domain, seed=0)
-        spec = synth.PROGRAMS[program]
-        sc = [v for _, v in spec.scalars]
+def program_measure(oec, torch, program, domain, l2, peak, variant=0, reps=20):
+    """us per launch of one program (CUDA graph of R launches over R rotating input sets > 4x L2)."""
+    host = synth.make_inputs(program, domain, seed=0)
+    spec = synth.PROGRAMS[program]
+    sc = [v for _, v in spec.scalars]
 
-        def make():
-            ins = [oec.field_from_host(host[s.name]) for s in spec.inputs]
-            outs = [oec.empty_like_domain(domain, fill=0.0) for _ in spec.outputs]
-            return ins, outs
+    def make():
+        ins = [oec.field_from_host(host[s.name]) for s in spec.inputs]
+        outs = [oec.empty_like_domain(domain, fill=0.0) for _ in spec.outputs]
+        return ins, outs
 
-        s0 = make()
-        set_bytes = sum(int(np.prod([f.ub[d] - f.lb[d] for d in range(3)])) * 8 for f in s0[0] + s0[1])
-        R = max(2, math.ceil(4 * l2 / set_bytes) + 1)
-        sets = [s0] + [make() for _ in range(R - 1)]
+    s0 = make()
+    set_bytes = sum(int(np.prod([f.ub[d] - f.lb[d] for d in range(3)])) * 8 for f in s0[0] + s0[1])
+    R = max(2, math.ceil(4 * l2 / set_bytes) + 1)
+    sets = [s0] + [make() for _ in range(R - 1)]
+    for ins, outs in sets:  # also sizes any library workspace outside the capture
+        oec.oec_apply_program(program, ins, outs, sc, (0, 0, 0), domain, variant)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
         for ins, outs in sets:
-            oec.oec_apply_program(program, ins, outs, sc, (0, 0, 0), domain)
-        torch.cuda.synchronize()
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g):
-            for ins, outs in sets:
-                oec.oec_apply_program(program, ins, outs, sc, (0, 0, 0), domain)
+            oec.oec_apply_program(program, ins, outs, sc, (0, 0, 0), domain, variant)
+    g.replay()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(reps):
         g.replay()
-        torch.cuda.synchronize()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record()
-        for _ in range(reps):
-            g.replay()
-        b.record()
-        torch.cuda.synchronize()
-        us = 1e3 * a.elapsed_time(b) / (reps * R)
-        nbytes = program_bytes(program, domain)
-        res[program] = {"us_per_launch": us, "algorithmic_bytes": nbytes, "GB/s": nbytes / (us * 1e-6) / 1e9,
-                        "frac_of_hbm_peak": nbytes / (us * 1e-6) / 1e9 / peak,
-                        "grid_points_per_s": domain[0] * domain[1] * domain[2] / (us * 1e-6)}
-        del sets, s0, g
+    b.record()
+    torch.cuda.synchronize()
+    us = 1e3 * a.elapsed_time(b) / (reps * R)
+    nbytes = program_bytes(program, domain)
+    del sets, s0, g
+    return {"us_per_launch": us, "algorithmic_bytes": nbytes, "GB/s": nbytes / (us * 1e-6) / 1e9,
+            "frac_of_hbm_peak": nbytes / (us * 1e-6) / 1e9 / peak,
+            "grid_points_per_s": domain[0] * domain[1] * domain[2] / (us * 1e-6)}
+
+
+def suite_measure(oec, torch, domain, l2, peak):
+    return {p: program_measure(oec, torch, p, domain, l2, peak) for p in synth.SUITE}
+
+
+def levels_measure(oec, torch, domain, l2, peak):
+    """The paper's optimisation-level experiment (Fig. 11) on B200: "original" (one kernel
+    per operator, temporaries in HBM) vs "inline" in the paper's execution model (one thread per
+    point, producers recomputed) vs this repo's default kernels."""
+    res = {}
+    for program, variants in (("hdiff", (("original", 1), ("inline_paper_model", 2), ("b200", 0))),
+                              ("vadv", (("original", 1), ("b200", 0)))):
+        r = {name: program_measure(oec, torch, program, domain, l2, peak, v) for name, v in variants}
+        base = r["original"]["us_per_launch"]
+        for name in r:
+            r[name]["speedup_over_original"] = base / r[name]["us_per_launch"]
+        res[program] = r
     return res
 
 

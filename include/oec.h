@@ -72,10 +72,15 @@ typedef enum { OEC_F64 = 0 } oec_dtype;
 
 /* Kernel variants of oec_apply_program / oec_hdiff_variant.                                   */
 typedef enum {
-    OEC_VARIANT_AUTO = 0,  /* fastest B200 kernel (default)                                     */
-    OEC_VARIANT_NAIVE = 2  /* the paper's execution model: one thread per point, every producer
-                              inlined and recomputed, registers only, no shared memory and no
-                              synchronisation -- kept for comparison            */
+    OEC_VARIANT_AUTO = 0,    /* fastest B200 kernel (default)                                   */
+    OEC_VARIANT_UNFUSED = 1, /* the paper's "original" level: one kernel per stencil
+                                operator, every intermediate materialised in HBM over its
+                                inferred range; hdiff and vadv only (others return
+                                OEC_ERR_UNSUPPORTED); uses a library-owned device workspace,
+                                grown on first use -- call once outside stream capture        */
+    OEC_VARIANT_NAIVE = 2    /* the paper's execution model: one thread per point, every producer
+                                inlined and recomputed, registers only, no shared memory and no
+                                synchronisation; for vadv the same as AUTO      */
 } oec_variant;
 
 typedef struct oec_field {

@@ -33,6 +33,11 @@ void hdiff_tma_boxes(int box_in[3], int box_cf[3]);
 cudaError_t launch_vadv(const FV &u_stage, const FV &wcon, const FV &u_pos, const FV &utens, const FV &usi,
                         const FO &out, double dtr, const Dom &d, const TMap *tmaps, cudaStream_t s, int *launches);
 void vadv_tma_boxes(const Dom &d, int box[3], int box_wc[3], int box_us[3], bool *fits);
+// the paper's "original" level: one kernel per operator, temporaries in HBM (csrc/unfused.cu)
+cudaError_t launch_hdiff_unfused(const FV &in, const FV &coeff, const FO &out, const Dom &d, cudaStream_t s,
+                                 int *launches);
+cudaError_t launch_vadv_unfused(const FV &us, const FV &wc, const FV &up, const FV &ut, const FV &usi, const FO &out,
+                                double dtr, const Dom &d, cudaStream_t s, int *launches);
 // suite: inputs / outputs in registry order
 cudaError_t launch_suite(int program_id, const FV *in, const FO *out, const double *scalars, const Dom &d,
                          cudaStream_t s, int *launches);

@@ -316,6 +316,13 @@ static oec_status run_device(int p, const oec_field *const *in, oec_field *const
     aligned16 = aligned16 && (d.lo[0] % 2 == 0);
     int launches = 0;
     cudaError_t e;
+    if (variant == OEC_VARIANT_UNFUSED) {
+        if (p == OEC_PROG_HDIFF) e = launch_hdiff_unfused(v_in[0], v_in[1], v_out[0], d, s, &launches);
+        else e = launch_vadv_unfused(v_in[0], v_in[1], v_in[2], v_in[3], v_in[4], v_out[0], sc[0], d, s, &launches);
+        if (e != cudaSuccess) return set_error(OEC_ERR_CUDA, "%s (unfused): %s", P.name, cudaGetErrorString(e));
+        g_launches = launches;
+        return OEC_OK;
+    }
     switch (p) {
     case OEC_PROG_HDIFF: {
         TMap tin, tcf;
@@ -356,8 +363,10 @@ static oec_status apply(int p, const oec_field *const *in, int n_in, oec_field *
     if (!in || !out) return set_error(OEC_ERR_ARG, "%s: NULL input/output array", P.name);
     if (n_sc != 0 && n_sc != P.n_sc) return set_error(OEC_ERR_ARG, "%s: expects %d scalars, got %d", P.name, P.n_sc, n_sc);
     if (n_sc && !scalars) return set_error(OEC_ERR_ARG, "%s: NULL scalars", P.name);
-    if (variant != OEC_VARIANT_AUTO && variant != OEC_VARIANT_NAIVE)
+    if (variant != OEC_VARIANT_AUTO && variant != OEC_VARIANT_NAIVE && variant != OEC_VARIANT_UNFUSED)
         return set_error(OEC_ERR_ARG, "%s: unknown variant %d", P.name, variant);
+    if (variant == OEC_VARIANT_UNFUSED && p != OEC_PROG_HDIFF && p != OEC_PROG_VADV)
+        return set_error(OEC_ERR_UNSUPPORTED, "%s: the unfused (original) variant exists for hdiff and vadv only", P.name);
     oec_status st = check_domain(lo, hi);
     if (st) return st;
     int device = -2;

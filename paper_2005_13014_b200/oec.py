@@ -23,6 +23,7 @@ OEC_OK = 0
 OEC_DEVICE_HOST = -1
 OEC_F64 = 0
 OEC_VARIANT_AUTO = 0
+OEC_VARIANT_UNFUSED = 1
 OEC_VARIANT_NAIVE = 2
 STATUS = {0: "OK", 1: "ERR_ARG", 2: "ERR_SHAPE", 3: "ERR_ALIAS", 4: "ERR_DTYPE", 5: "ERR_CUDA", 6: "ERR_NCCL",
           7: "ERR_UNSUPPORTED", 8: "ERR_LAYOUT"}

@@ -234,3 +234,12 @@ def test_vadv_odd_pitch_register_kernel():
     torch.cuda.synchronize()
     r = run_oracle("vadv", host, domain)
     _assert_parity(t_out.cpu().numpy(), r["utens_stage_out"], "vadv odd pitch")
+
+
+@pytest.mark.parametrize("program", ["hdiff", "vadv"])
+@pytest.mark.parametrize("domain", [(33, 31, 5), (128, 128, 80)])
+def test_unfused_original_level(program, domain):
+    # OEC_VARIANT_UNFUSED: the paper's "original" level (one kernel per operator, temporaries in HBM)
+    # computes the same values bit for bit
+    _check(program, domain, seed=2, variant=1)
+    _check(program, domain, seed=2, variant=1, dom_lb=(1, 2, 0), dom_ub=(domain[0] - 3, domain[1] - 1, domain[2]))
