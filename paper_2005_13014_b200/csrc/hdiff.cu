@@ -28,17 +28,56 @@
 #include "oec_internal.h"
 #include "tma.h"
 
+// Two tile configurations (measured sweeps in profiles/ncu_summary_r01.md): small domains want
+// many short tiles per SM (V=2: 64 columns, JB=4 rows, 12 warps x 2 slots); large domains want
+// wide 2-row tiles (V=4: 128 columns) -- more independent warps in flight per SM.
 #ifndef HD_V
 #define HD_V 2
 #endif
 #ifndef HD_JB
-#define HD_JB 8
+#define HD_JB 4
 #endif
 #ifndef HD_S
-#define HD_S 3
+#define HD_S 2
 #endif
 #ifndef HD_NW
-#define HD_NW 6
+#define HD_NW 12
+#endif
+#ifndef HDL_V
+#define HDL_V 4
+#endif
+#ifndef HDL_JB
+#define HDL_JB 2
+#endif
+#ifndef HDL_S
+#define HDL_S 2
+#endif
+#ifndef HDL_NW
+#define HDL_NW 12
+#endif
+#ifndef HD_LARGE_POINTS
+#define HD_LARGE_POINTS (2ll << 20)
+#endif
+
+#ifdef HD_TRACE
+// debug timeline of CTA 0 and CTA gridDim-1: [cta(0/1)][warp][event]: 0 start, 1+2n item n data ready, 2+2n item n done
+__device__ unsigned long long g_htrace[2][8][64];
+extern "C" int oec_debug_hdiff_trace(unsigned long long *out) {
+    return (int)cudaMemcpyFromSymbol(out, g_htrace, sizeof(g_htrace));
+}
+#define HTRACE(ev)                                                                                         \
+    do {                                                                                                   \
+        const int c_ = blockIdx.x == 0 ? 0 : (blockIdx.x == gridDim.x - 1 ? 1 : -1);                        \
+        if (c_ >= 0 && (threadIdx.x & 31) == 0 && (ev) < 64) {                                             \
+            unsigned long long t_;                                                                         \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                                          \
+            g_htrace[c_][threadIdx.x >> 5][ev] = t_;                                                        \
+        }                                                                                                  \
+    } while (0)
+#else
+#define HTRACE(ev) \
+    do {           \
+    } while (0)
 #endif
 
 namespace oec {
@@ -95,7 +134,7 @@ struct Vec<2> {
 };
 
 template <>
-struct __attribute__((unused)) Vec<4> {
+struct Vec<4> {
     static __device__ __forceinline__ void load(const double *p, double *v) {
         Vec<2>::load(p, v);
         Vec<2>::load(p + 2, v + 2);
@@ -412,12 +451,17 @@ __global__ void __launch_bounds__(NW * 32, 1) hdiff_tma(const __grid_constant__ 
         tma_load_ijk(cf_s(s), m_cf, &bars[s], ib, j0, k);
     };
 
+    HTRACE(0);
+    griddep_launch_dependents();
     if (lane == 0) {
         prefetch_tmap(&m_in.map);
         prefetch_tmap(&m_cf.map);
 #pragma unroll
         for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
         fence_mbar_init();
+    }
+    griddep_wait();  // inputs may be the previous kernel's outputs
+    if (lane == 0) {
 #pragma unroll
         for (int s = 0; s < S; ++s)
             if (gw + s * nwt < nitems) issue(gw + s * nwt, s);
@@ -433,11 +477,13 @@ __global__ void __launch_bounds__(NW * 32, 1) hdiff_tma(const __grid_constant__ 
         const int i_own = ib + lane * V;
         double *out_k = out.p + k * out.sk;
         mbar_wait(&bars[s], (n / S) & 1);
+        HTRACE(1 + 2 * n);
         if (nrows == JB)
             hdiff_tile<V, JB, true>(in_s(s), cf_s(s), out_k, out.sj, j0, JB, i_own, d.hi[0], lane);
         else
             hdiff_tile<V, JB, false>(in_s(s), cf_s(s), out_k, out.sj, j0, nrows, i_own, d.hi[0], lane);
         __syncwarp();
+        HTRACE(2 + 2 * n);
         if (lane == 0) {
             const int nxt = item + S * nwt;
             if (nxt < nitems) {
@@ -468,9 +514,10 @@ cudaError_t launch_tma(const TMap &tin, const TMap &tcf, const FO &out, const Do
         configured = true;
     }
     long long blocks = std::min<long long>((nitems + NW - 1) / NW, (long long)sms * blocks_per_sm);
-    hdiff_tma<V, JB, S, NW><<<(unsigned)blocks, NW * 32, C::SMEM, st>>>(tin, tcf, out, d, nseg, nchunk, (int)nitems);
+    cudaError_t e = launch_pdl(hdiff_tma<V, JB, S, NW>, dim3((unsigned)blocks), dim3(NW * 32), C::SMEM, st, tin, tcf, out,
+                               d, nseg, nchunk, (int)nitems);
     ++*launches;
-    return cudaGetLastError();
+    return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 template <int V, int JB, int P>
@@ -488,12 +535,18 @@ cudaError_t launch_roll(const FV &in, const FV &coeff, const FO &out, const Dom 
 
 }  // namespace
 
-void hdiff_tma_boxes(int box_in[3], int box_cf[3]) {
-    box_in[0] = 32 * HD_V + 4;
-    box_in[1] = HD_JB + 4;
+static bool hdiff_large(const Dom &d) {
+    return (long long)(d.hi[0] - d.lo[0]) * (d.hi[1] - d.lo[1]) * (d.hi[2] - d.lo[2]) >= HD_LARGE_POINTS;
+}
+
+void hdiff_tma_boxes(const Dom &d, int box_in[3], int box_cf[3]) {
+    const bool L = hdiff_large(d);
+    const int V = L ? HDL_V : HD_V, JB = L ? HDL_JB : HD_JB;
+    box_in[0] = 32 * V + 4;
+    box_in[1] = JB + 4;
     box_in[2] = 1;
-    box_cf[0] = 32 * HD_V;
-    box_cf[1] = HD_JB;
+    box_cf[0] = 32 * V;
+    box_cf[1] = JB;
     box_cf[2] = 1;
 }
 
@@ -506,7 +559,10 @@ cudaError_t launch_hdiff(const FV &in, const FV &coeff, const FO &out, const Dom
         ++*launches;
         return cudaGetLastError();
     }
-    if (tin && tcf && aligned16) return launch_tma<HD_V, HD_JB, HD_S, HD_NW>(*tin, *tcf, out, d, s, launches);
+    if (tin && tcf && aligned16) {
+        if (hdiff_large(d)) return launch_tma<HDL_V, HDL_JB, HDL_S, HDL_NW>(*tin, *tcf, out, d, s, launches);
+        return launch_tma<HD_V, HD_JB, HD_S, HD_NW>(*tin, *tcf, out, d, s, launches);
+    }
     if (aligned16) return launch_roll<2, 16, 4>(in, coeff, out, d, s, launches);
     return launch_roll<1, 16, 4>(in, coeff, out, d, s, launches);
 }

@@ -29,7 +29,7 @@ struct Dom {
 // launchers (return cudaGetLastError() of their launches); `launches` is incremented per launch
 cudaError_t launch_hdiff(const FV &in, const FV &coeff, const FO &out, const Dom &d, int variant, bool aligned16,
                          const TMap *tin, const TMap *tcf, cudaStream_t s, int *launches);
-void hdiff_tma_boxes(int box_in[3], int box_cf[3]);
+void hdiff_tma_boxes(const Dom &d, int box_in[3], int box_cf[3]);
 cudaError_t launch_vadv(const FV &u_stage, const FV &wcon, const FV &u_pos, const FV &utens, const FV &usi,
                         const FO &out, double dtr, const Dom &d, const TMap *tmaps, cudaStream_t s, int *launches);
 void vadv_tma_boxes(const Dom &d, int box[3], int box_wc[3], int box_us[3], bool *fits);

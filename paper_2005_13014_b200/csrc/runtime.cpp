@@ -327,7 +327,7 @@ static oec_status run_device(int p, const oec_field *const *in, oec_field *const
     case OEC_PROG_HDIFF: {
         TMap tin, tcf;
         int bin[3], bcf[3];
-        hdiff_tma_boxes(bin, bcf);
+        hdiff_tma_boxes(d, bin, bcf);
         const bool tma = variant == OEC_VARIANT_AUTO && make_tmap(in[0], bin, &tin) && make_tmap(in[1], bcf, &tcf);
         e = launch_hdiff(v_in[0], v_in[1], v_out[0], d, variant, aligned16, tma ? &tin : nullptr, tma ? &tcf : nullptr,
                          s, &launches);

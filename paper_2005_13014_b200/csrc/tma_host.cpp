@@ -1,5 +1,6 @@
 // Host side of tma.h: encode a 3D tensor map over an oec_field's allocation.
 #include <cudaTypedefs.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <mutex>
@@ -17,6 +18,15 @@ static void load_encode() {
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
         q == cudaDriverEntryPointSuccess)
         g_encode = (PFN_cuTensorMapEncodeTiled_v12000)fn;
+}
+
+bool pdl_enabled() {
+    static int on = -1;
+    if (on < 0) {
+        const char *e = getenv("OEC_PDL");
+        on = (e && e[0] == '0') ? 0 : 1;
+    }
+    return on == 1;
 }
 
 bool make_tmap(const oec_field *f, const int box[3], TMap *out) {

@@ -243,3 +243,9 @@ def test_unfused_original_level(program, domain):
     # computes the same values bit for bit
     _check(program, domain, seed=2, variant=1)
     _check(program, domain, seed=2, variant=1, dom_lb=(1, 2, 0), dom_ub=(domain[0] - 3, domain[1] - 1, domain[2]))
+
+
+def test_hdiff_large_config_ragged():
+    # >= 2M points selects the wide-tile hdiff configuration (V=4, JB=2); ragged in i and j
+    _check("hdiff", (1031, 1029, 3), seed=5)
+    _check("hdiff", (333, 6301, 1), seed=6, out_halo=(2, 2, 0))
