@@ -208,7 +208,11 @@ __global__ void __launch_bounds__(SU_BX * SU_BY) suite_kernel(const __grid_const
     const int i = a.d.lo[0] + blockIdx.x * SU_BX + threadIdx.x;
     const int j = a.d.lo[1] + blockIdx.y * SU_BY + threadIdx.y;
     const int k0 = a.d.lo[2] + blockIdx.z * KC;
-    if (i >= a.d.hi[0] || j >= a.d.hi[1]) return;
+    griddep_wait();  // PDL: inputs may be the previous kernel's outputs
+    if (i >= a.d.hi[0] || j >= a.d.hi[1]) {
+        griddep_launch_dependents();
+        return;
+    }
     double r[KC][NO];
 #pragma unroll
     for (int kk = 0; kk < KC; ++kk) F(a.in, a.sc, i, j, min(k0 + kk, a.d.hi[2] - 1), r[kk]);
@@ -218,6 +222,7 @@ __global__ void __launch_bounds__(SU_BX * SU_BY) suite_kernel(const __grid_const
 #pragma unroll
             for (int o = 0; o < NO; ++o) a.out[o].p[i + j * a.out[o].sj + (k0 + kk) * a.out[o].sk] = r[kk][o];
         }
+    griddep_launch_dependents();  // late: dependents launched early would idle in griddepcontrol.wait
 }
 
 }  // namespace
@@ -234,18 +239,19 @@ cudaError_t launch_suite(int program_id, const FV *in, const FO *out, const doub
     dim3 block(SU_BX, SU_BY, 1);
     dim3 grid((d.hi[0] - d.lo[0] + SU_BX - 1) / SU_BX, (d.hi[1] - d.lo[1] + SU_BY - 1) / SU_BY,
               (d.hi[2] - d.lo[2] + KC - 1) / KC);
+    cudaError_t e = cudaSuccess;
     switch (program_id) {
-    case OEC_PROG_UVBKE: suite_kernel<uvbke_pt, 2, KC><<<grid, block, 0, s>>>(a); break;
-    case OEC_PROG_P_GRAD_C: suite_kernel<p_grad_c_pt, 2, KC><<<grid, block, 0, s>>>(a); break;
-    case OEC_PROG_NH_P_GRAD: suite_kernel<nh_p_grad_pt, 2, KC><<<grid, block, 0, s>>>(a); break;
-    case OEC_PROG_FVTP2D_QI: suite_kernel<fvtp2d_qi_pt, 2, KC><<<grid, block, 0, s>>>(a); break;
-    case OEC_PROG_FVTP2D_QJ: suite_kernel<fvtp2d_qj_pt, 3, KC><<<grid, block, 0, s>>>(a); break;
-    case OEC_PROG_FVTP2D_FLUX: suite_kernel<fvtp2d_flux_pt, 2, KC><<<grid, block, 0, s>>>(a); break;
-    case OEC_PROG_FASTWAVES: suite_kernel<fastwaves_pt, 2, KC><<<grid, block, 0, s>>>(a); break;
+    case OEC_PROG_UVBKE: e = launch_pdl(suite_kernel<uvbke_pt, 2, KC>, grid, block, 0, s, a); break;
+    case OEC_PROG_P_GRAD_C: e = launch_pdl(suite_kernel<p_grad_c_pt, 2, KC>, grid, block, 0, s, a); break;
+    case OEC_PROG_NH_P_GRAD: e = launch_pdl(suite_kernel<nh_p_grad_pt, 2, KC>, grid, block, 0, s, a); break;
+    case OEC_PROG_FVTP2D_QI: e = launch_pdl(suite_kernel<fvtp2d_qi_pt, 2, KC>, grid, block, 0, s, a); break;
+    case OEC_PROG_FVTP2D_QJ: e = launch_pdl(suite_kernel<fvtp2d_qj_pt, 3, KC>, grid, block, 0, s, a); break;
+    case OEC_PROG_FVTP2D_FLUX: e = launch_pdl(suite_kernel<fvtp2d_flux_pt, 2, KC>, grid, block, 0, s, a); break;
+    case OEC_PROG_FASTWAVES: e = launch_pdl(suite_kernel<fastwaves_pt, 2, KC>, grid, block, 0, s, a); break;
     default: return cudaErrorInvalidValue;
     }
     ++*launches;
-    return cudaGetLastError();
+    return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 }  // namespace oec

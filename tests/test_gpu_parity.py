@@ -249,3 +249,4 @@ def test_hdiff_large_config_ragged():
     # >= 2M points selects the wide-tile hdiff configuration (V=4, JB=2); ragged in i and j
     _check("hdiff", (1031, 1029, 3), seed=5)
     _check("hdiff", (333, 6301, 1), seed=6, out_halo=(2, 2, 0))
+    _check("hdiff", (517, 1000, 5), seed=7, order=(0, 1, 2))
