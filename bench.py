@@ -253,6 +253,8 @@ def main():
     ap.add_argument("--no-suite", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--sets", type=int, default=0, help="rotating input sets (0 = auto, > 4x L2)")
+    ap.add_argument("--force-decomp", action="store_true",
+                    help="debug: run the N>1 code path (NCCL process group, decomposition, exchange) even at N=1")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -269,7 +271,13 @@ def main():
     oec.lib()  # fail loudly if the extension is missing
     torch.cuda.set_device(local_rank)
     dev = torch.cuda.current_device()
-    if world > 1:
+    decomp = world > 1 or args.force_decomp
+    if decomp:
+        if world == 1:
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29517")
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     props = torch.cuda.get_device_properties(dev)
     l2 = int(getattr(props, "L2_cache_size", 126 * 2**20))
@@ -278,14 +286,14 @@ def main():
 
     # ---- decomposition (N > 1): j-slabs of the global 128 x 128N x 80 domain ----
     dec = None
-    if world > 1:
+    if decomp:
         from torch._C._distributed_c10d import ProcessGroupNCCL
 
         pg = dist.distributed_c10d._get_default_group()
         nccl_pg = pg._get_backend(torch.device("cuda", local_rank))
         dist.barrier()
-        comm = nccl_pg._comm_ptr()
-        dec = oec.oec_decomp_create((domain[0], domain[1] * world, domain[2]), 1, world, rank, comm)
+        nccl_comm = nccl_pg._comm_ptr()
+        dec = oec.oec_decomp_create((domain[0], domain[1] * world, domain[2]), 1, world, rank, nccl_comm)
 
     # ---- rotating input sets ----
     hh = synth.make_inputs("hdiff", domain, seed=rank)
@@ -308,6 +316,7 @@ def main():
     def exchange(s):
         if dec is not None:
             oec.oec_halo_exchange(dec, [s.h_in], (2, 2, 0), (2, 2, 0))
+            launches["halo"] = oec.oec_last_launch_count()
 
     # warm-up (also configures kernel attributes and NCCL staging before any capture)
     for w in range(args.warmup):
@@ -318,10 +327,15 @@ def main():
     torch.cuda.synchronize()
 
     # ---- CUDA graphs of R launches of each kernel (launch-overhead-free timing) ----
-    use_graphs = world == 1
+    # N > 1: the hdiff halo exchange (NCCL, comm stream) runs concurrently with vadv (no halo
+    # needed for j-slabs), then hdiff; graphs gx (exchanges), gv (vadv), gh (hdiff) per R steps.
+    has_x = dec is not None
+    comm_stream = torch.cuda.Stream() if has_x else None
     graphs = {}
+    x_mode = None
 
     def capture(nsteps):
+        nonlocal x_mode
         gh, gv = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
         with torch.cuda.graph(gh):
             for q in range(nsteps):
@@ -329,16 +343,28 @@ def main():
         with torch.cuda.graph(gv):
             for q in range(nsteps):
                 vadv(sets[q % R])
-        return gh, gv
+        gx = None
+        if has_x:
+            try:
+                gx = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(gx):
+                    for q in range(nsteps):
+                        exchange(sets[q % R])
+                x_mode = "NCCL captured in a CUDA graph on a comm stream, concurrent with vadv"
+            except Exception as e:  # NCCL capture unavailable: exchanges launched eagerly instead
+                gx = None
+                x_mode = f"NCCL launched eagerly on a comm stream, concurrent with vadv ({type(e).__name__})"
+        return gh, gv, gx
 
-    if use_graphs:
-        graphs[R] = capture(R)
-        if args.steps % R:
-            graphs[args.steps % R] = capture(args.steps % R)
-        for g in graphs.values():  # one untimed replay each
-            g[0].replay()
-            g[1].replay()
-        torch.cuda.synchronize()
+    graphs[R] = capture(R)
+    if args.steps % R:
+        graphs[args.steps % R] = capture(args.steps % R)
+    for g in graphs.values():  # one untimed replay each
+        g[0].replay()
+        g[1].replay()
+        if g[2] is not None:
+            g[2].replay()
+    torch.cuda.synchronize()
 
     chunks = [R] * (args.steps // R) + ([args.steps % R] if args.steps % R else [])
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
@@ -353,31 +379,32 @@ def main():
     t_stop = torch.cuda.Event(enable_timing=True)
     t_start.record()
     done = 0
+    cur = torch.cuda.current_stream()
     for c, n in enumerate(chunks):
         e0, e1, e2 = ev[c]
-        if use_graphs:
-            e0.record()
-            graphs[n][0].replay()
-            e1.record()
-            graphs[n][1].replay()
-            e2.record()
-        else:
-            e0.record()
-            for q in range(n):
-                s = sets[(done + q) % R]
-                exchange(s)
-                hdiff(s)
-            e1.record()
-            for q in range(n):
-                vadv(sets[(done + q) % R])
-            e2.record()
+        gh, gv, gx = graphs[n]
+        e0.record()
+        if has_x:
+            comm_stream.wait_stream(cur)
+            with torch.cuda.stream(comm_stream):
+                if gx is not None:
+                    gx.replay()
+                else:
+                    for q in range(n):
+                        exchange(sets[(done + q) % R])
+        gv.replay()
+        if has_x:
+            cur.wait_stream(comm_stream)
+        e1.record()
+        gh.replay()
+        e2.record()
         done += n
     t_stop.record()
     torch.cuda.synchronize()
     clocks.mark_stop()
     elapsed_ms = t_start.elapsed_time(t_stop)
-    t_h = sum(e[0].elapsed_time(e[1]) for e in ev)
-    t_v = sum(e[1].elapsed_time(e[2]) for e in ev)
+    t_v = sum(e[0].elapsed_time(e[1]) for e in ev)  # vadv (|| halo exchange when N > 1)
+    t_h = sum(e[1].elapsed_time(e[2]) for e in ev)
     if world > 1:
         t = torch.tensor([elapsed_ms, t_h, t_v], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -416,7 +443,7 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_baseline(domain, args.cpu_seconds)
 
-    n_launch = K * (launches["hdiff"] + launches["vadv"])
+    n_launch = K * (launches["hdiff"] + launches["vadv"] + launches["halo"])
     if rank == 0:
         res = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": args.warmup,
@@ -427,8 +454,8 @@ def main():
                        "parallelism": f"j-slab decomposition 1x{world}, NCCL halo exchange" if world > 1 else "single GPU",
                        "l2": f"inputs larger than L2: {R} rotating input sets, "
                              f"{R * first.nbytes() / 2**20:.0f} MiB total vs {l2 / 2**20:.0f} MiB L2",
-                       "timing": "CUDA events on the launching stream; CUDA graphs of R launches" if use_graphs
-                       else "CUDA events, eager launches, max over ranks"},
+                       "timing": "CUDA events on the launching stream around CUDA graphs of R launches per "
+                                 "kernel; max over ranks" + (f"; halo exchange: {x_mode}" if has_x else "")},
             "roofline": roofline,
             "kernels": kern,
             "cpu_baseline": cpu,
@@ -441,7 +468,7 @@ def main():
         if levels is not None:
             res["optimization_levels"] = levels
         print(json.dumps(res), flush=True)
-    if world > 1:
+    if decomp:
         dist.barrier()
         dist.destroy_process_group()
     return 0

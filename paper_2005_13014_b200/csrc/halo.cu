@@ -266,6 +266,7 @@ oec_status oec_halo_exchange(oec_decomp *d, oec_field *const *fields, int32_t n,
     oec_status st = check_widths(width_lo, width_hi);
     if (st) return st;
     auto plan = make_plan(d->gdom, d->px, d->py, d->rank, width_lo, width_hi);
+    set_launch_count(0);
     if (plan.empty() || n == 0) return OEC_OK;
     if (!d->comm) return set_error(OEC_ERR_NCCL, "oec_halo_exchange: decomposition has no NCCL communicator");
     if (!load_nccl()) return set_error(OEC_ERR_NCCL, "oec_halo_exchange: libnccl.so.2 not loadable in this process");
@@ -326,6 +327,7 @@ oec_status oec_halo_exchange(oec_decomp *d, oec_field *const *fields, int32_t n,
                     if (e != cudaSuccess) return set_error(OEC_ERR_CUDA, "halo unpack: %s", cudaGetErrorString(e));
                 }
     }
+    set_launch_count(launches);
     return OEC_OK;
 }
 
@@ -363,6 +365,7 @@ oec_status oec_halo_exchange_local(const int64_t global_domain[3], int32_t px, i
             }
         }
     }
+    set_launch_count(launches);
     return OEC_OK;
 }
 

@@ -50,8 +50,9 @@ cudaError_t launch_pack(const FV &src, const Box &b, double *buf, cudaStream_t s
 cudaError_t launch_unpack(const double *buf, const Box &b, const FO &dst, cudaStream_t s, int *launches);
 cudaError_t launch_box_copy(const FV &src, const FO &dst, const Box &b, cudaStream_t s, int *launches);
 
-// error plumbing
+// error plumbing; launch count reported by oec_last_launch_count
 oec_status set_error(oec_status st, const char *fmt, ...);
+void set_launch_count(int n);
 
 }  // namespace oec
 
