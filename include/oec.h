@@ -70,17 +70,24 @@ typedef enum {
 
 typedef enum { OEC_F64 = 0 } oec_dtype;
 
-/* Kernel variants of oec_apply_program / oec_hdiff_variant.                                   */
+/* Kernel variants of oec_apply_program / oec_hdiff_variant: the paper's optimisation levels
+   (§7.3: original, inline, inline+unroll(2), inline+unroll(4)) plus the tuned
+   B200 kernels.  All variants produce bit-identical results.                                   */
 typedef enum {
     OEC_VARIANT_AUTO = 0,    /* fastest B200 kernel (default)                                   */
-    OEC_VARIANT_UNFUSED = 1, /* the paper's "original" level: one kernel per stencil
-                                operator, every intermediate materialised in HBM over its
-                                inferred range; hdiff and vadv only (others return
-                                OEC_ERR_UNSUPPORTED); uses a library-owned device workspace,
-                                grown on first use -- call once outside stream capture        */
-    OEC_VARIANT_NAIVE = 2    /* the paper's execution model: one thread per point, every producer
-                                inlined and recomputed, registers only, no shared memory and no
-                                synchronisation; for vadv the same as AUTO      */
+    OEC_VARIANT_UNFUSED = 1, /* "original": one kernel per stencil.apply, every
+                                intermediate materialised in HBM over its inferred range
+                                (P:480-482); uses a library-owned device workspace, grown on
+                                first use -- call once outside stream capture                  */
+    OEC_VARIANT_NAIVE = 2,   /* "inline" in the paper's execution model: one thread per point
+                                (vadv: per column, sequential in k), every producer inlined and
+                                recomputed, registers only, no synchronisation  */
+    OEC_VARIANT_UNROLL2 = 3, /* "inline+unroll(2)": NAIVE with stencil unrolling by 2 along j
+                                (P:447-454): one thread updates two rows, shared loads and
+                                producer evaluations computed once.  Not for vadv
+                                (OEC_ERR_UNSUPPORTED: unrolling does not apply to the column
+                                solver)                                                        */
+    OEC_VARIANT_UNROLL4 = 4  /* "inline+unroll(4)": as UNROLL2 with factor 4                    */
 } oec_variant;
 
 typedef struct oec_field {

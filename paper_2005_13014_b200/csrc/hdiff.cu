@@ -94,21 +94,32 @@ __device__ __forceinline__ double limit(double f, double din) { return (f * din 
 // ---------------------------------------------------------------------------------------------
 // paper execution model
 // ---------------------------------------------------------------------------------------------
+// UJ > 1: stencil unrolling along j: one thread updates UJ consecutive rows; the
+// Laplacians and loads the rows share are computed once (common-subexpression elimination).
+template <int UJ>
 __global__ void __launch_bounds__(128) hdiff_naive(FV in, FV coeff, FO out, Dom d) {
     const int i = d.lo[0] + blockIdx.x * 32 + threadIdx.x;
-    const int j = d.lo[1] + blockIdx.y * 4 + threadIdx.y;
+    const int j0 = d.lo[1] + (blockIdx.y * 4 + threadIdx.y) * UJ;
     const int k = d.lo[2] + blockIdx.z;
-    if (i >= d.hi[0] || j >= d.hi[1]) return;
+    if (i >= d.hi[0] || j0 >= d.hi[1]) return;
     auto L = [&](int a, int b) {
         return lap_pt(ld(in, a, b, k), ld(in, a - 1, b, k), ld(in, a + 1, b, k), ld(in, a, b - 1, k), ld(in, a, b + 1, k));
     };
-    const double c0 = ld(in, i, j, k);
-    const double l0 = L(i, j), le = L(i + 1, j), lw = L(i - 1, j), ln = L(i, j + 1), ls = L(i, j - 1);
-    const double flx = limit(le - l0, ld(in, i + 1, j, k) - c0);
-    const double flxm = limit(l0 - lw, c0 - ld(in, i - 1, j, k));
-    const double fly = limit(ln - l0, ld(in, i, j + 1, k) - c0);
-    const double flym = limit(l0 - ls, c0 - ld(in, i, j - 1, k));
-    out.p[i + j * out.sj + k * out.sk] = c0 - ld(coeff, i, j, k) * ((flx - flxm) + (fly - flym));
+    double r[UJ];
+#pragma unroll
+    for (int u = 0; u < UJ; ++u) {
+        const int j = min(j0 + u, d.hi[1] - 1);
+        const double c0 = ld(in, i, j, k);
+        const double l0 = L(i, j), le = L(i + 1, j), lw = L(i - 1, j), ln = L(i, j + 1), ls = L(i, j - 1);
+        const double flx = limit(le - l0, ld(in, i + 1, j, k) - c0);
+        const double flxm = limit(l0 - lw, c0 - ld(in, i - 1, j, k));
+        const double fly = limit(ln - l0, ld(in, i, j + 1, k) - c0);
+        const double flym = limit(l0 - ls, c0 - ld(in, i, j - 1, k));
+        r[u] = c0 - ld(coeff, i, j, k) * ((flx - flxm) + (fly - flym));
+    }
+#pragma unroll
+    for (int u = 0; u < UJ; ++u)
+        if (j0 + u < d.hi[1]) out.p[i + (j0 + u) * out.sj + k * out.sk] = r[u];
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -552,10 +563,13 @@ void hdiff_tma_boxes(const Dom &d, int box_in[3], int box_cf[3]) {
 
 cudaError_t launch_hdiff(const FV &in, const FV &coeff, const FO &out, const Dom &d, int variant, bool aligned16,
                          const TMap *tin, const TMap *tcf, cudaStream_t s, int *launches) {
-    if (variant == OEC_VARIANT_NAIVE) {
+    if (variant == OEC_VARIANT_NAIVE || variant == OEC_VARIANT_UNROLL2 || variant == OEC_VARIANT_UNROLL4) {
+        const int uj = variant == OEC_VARIANT_UNROLL4 ? 4 : variant == OEC_VARIANT_UNROLL2 ? 2 : 1;
         dim3 block(32, 4, 1);
-        dim3 grid((d.hi[0] - d.lo[0] + 31) / 32, (d.hi[1] - d.lo[1] + 3) / 4, d.hi[2] - d.lo[2]);
-        hdiff_naive<<<grid, block, 0, s>>>(in, coeff, out, d);
+        dim3 grid((d.hi[0] - d.lo[0] + 31) / 32, (d.hi[1] - d.lo[1] + 4 * uj - 1) / (4 * uj), d.hi[2] - d.lo[2]);
+        if (uj == 4) hdiff_naive<4><<<grid, block, 0, s>>>(in, coeff, out, d);
+        else if (uj == 2) hdiff_naive<2><<<grid, block, 0, s>>>(in, coeff, out, d);
+        else hdiff_naive<1><<<grid, block, 0, s>>>(in, coeff, out, d);
         ++*launches;
         return cudaGetLastError();
     }

@@ -38,9 +38,13 @@ cudaError_t launch_hdiff_unfused(const FV &in, const FV &coeff, const FO &out, c
                                  int *launches);
 cudaError_t launch_vadv_unfused(const FV &us, const FV &wc, const FV &up, const FV &ut, const FV &usi, const FO &out,
                                 double dtr, const Dom &d, cudaStream_t s, int *launches);
-// suite: inputs / outputs in registry order
+// suite: inputs / outputs in registry order; `unroll` = points per thread along j (1, 2, 4)
 cudaError_t launch_suite(int program_id, const FV *in, const FO *out, const double *scalars, const Dom &d,
-                         cudaStream_t s, int *launches);
+                         int unroll, cudaStream_t s, int *launches);
+// suite "original" level: one kernel per stencil.apply, temporaries in HBM (csrc/suite_unfused.cu)
+cudaError_t launch_suite_unfused(int program_id, int n_in, const FV *in, const FO *out, const double *scalars,
+                                 const Dom &d, cudaStream_t s, int *launches);
+int suite_unfused_stages(int program_id);
 
 // box copies for halo exchange: [lo, hi) box (absolute coords) between fields / packed buffers
 struct Box {

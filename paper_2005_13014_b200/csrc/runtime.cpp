@@ -294,6 +294,14 @@ static cudaError_t d2h_box(const oec_field *host, const oec_field *dev, const in
 // ---------------------------------------------------------------------------------------------
 // dispatch
 // ---------------------------------------------------------------------------------------------
+// AUTO's unroll factor per suite program: the paper picks it by empirical tuning; these are
+// the fastest of 1 / 2 / 4 measured on B200 at 128x128x80 (bench.py optimization_levels,
+// profiles/ncu_summary_r01.md)
+static int unroll_of(int p, int variant) {
+    if (variant == OEC_VARIANT_AUTO) return (p == OEC_PROG_UVBKE || p == OEC_PROG_FVTP2D_QI) ? 2 : 1;
+    return variant == OEC_VARIANT_UNROLL2 ? 2 : variant == OEC_VARIANT_UNROLL4 ? 4 : 1;
+}
+
 static oec_status run_device(int p, const oec_field *const *in, oec_field *const *out, const double *sc,
                              const int64_t *lo, const int64_t *hi, int variant, cudaStream_t s) {
     const ProgSpec &P = PROGS[p];
@@ -320,7 +328,9 @@ static oec_status run_device(int p, const oec_field *const *in, oec_field *const
     cudaError_t e;
     if (variant == OEC_VARIANT_UNFUSED) {
         if (p == OEC_PROG_HDIFF) e = launch_hdiff_unfused(v_in[0], v_in[1], v_out[0], d, s, &launches);
-        else e = launch_vadv_unfused(v_in[0], v_in[1], v_in[2], v_in[3], v_in[4], v_out[0], sc[0], d, s, &launches);
+        else if (p == OEC_PROG_VADV)
+            e = launch_vadv_unfused(v_in[0], v_in[1], v_in[2], v_in[3], v_in[4], v_out[0], sc[0], d, s, &launches);
+        else e = launch_suite_unfused(p, P.n_in, v_in, v_out, sc, d, s, &launches);
         if (e != cudaSuccess) return set_error(OEC_ERR_CUDA, "%s (unfused): %s", P.name, cudaGetErrorString(e));
         g_launches = launches;
         return OEC_OK;
@@ -347,7 +357,7 @@ static oec_status run_device(int p, const oec_field *const *in, oec_field *const
                         &launches);
         break;
     }
-    default: e = launch_suite(p, v_in, v_out, sc, d, s, &launches); break;
+    default: e = launch_suite(p, v_in, v_out, sc, d, unroll_of(p, variant), s, &launches); break;
     }
     if (e != cudaSuccess) return set_error(OEC_ERR_CUDA, "%s: kernel launch failed: %s", P.name, cudaGetErrorString(e));
     g_launches = launches;
@@ -365,10 +375,12 @@ static oec_status apply(int p, const oec_field *const *in, int n_in, oec_field *
     if (!in || !out) return set_error(OEC_ERR_ARG, "%s: NULL input/output array", P.name);
     if (n_sc != 0 && n_sc != P.n_sc) return set_error(OEC_ERR_ARG, "%s: expects %d scalars, got %d", P.name, P.n_sc, n_sc);
     if (n_sc && !scalars) return set_error(OEC_ERR_ARG, "%s: NULL scalars", P.name);
-    if (variant != OEC_VARIANT_AUTO && variant != OEC_VARIANT_NAIVE && variant != OEC_VARIANT_UNFUSED)
+    if (variant < OEC_VARIANT_AUTO || variant > OEC_VARIANT_UNROLL4)
         return set_error(OEC_ERR_ARG, "%s: unknown variant %d", P.name, variant);
-    if (variant == OEC_VARIANT_UNFUSED && p != OEC_PROG_HDIFF && p != OEC_PROG_VADV)
-        return set_error(OEC_ERR_UNSUPPORTED, "%s: the unfused (original) variant exists for hdiff and vadv only", P.name);
+    if ((variant == OEC_VARIANT_UNROLL2 || variant == OEC_VARIANT_UNROLL4) && p == OEC_PROG_VADV)
+        return set_error(OEC_ERR_UNSUPPORTED,
+                         "vadv: stencil unrolling (P:447) does not apply to the vertical solver (independent columns, "
+                         "no shared producers for CSE to remove)");
     oec_status st = check_domain(lo, hi);
     if (st) return st;
     int device = -2;

@@ -200,56 +200,69 @@ typedef void (*PointFn)(const FV *, const double *, int, int, int, double *);
 #define SU_KC 1
 #endif
 
-// One thread computes KC consecutive levels of one (i, j): every load of the KC levels is issued
-// before any store (outputs are kept in registers), so the loads overlap (memory-level
-// parallelism) and loads shared between levels (k+1 of level k = k of level k+1) are reused.
-template <PointFn F, int NO, int KC>
+// One thread computes KC consecutive levels and UJ consecutive rows of one i (stencil unrolling
+// along j: the operator is replicated per row, and the compiler's common-subexpression
+// elimination removes the loads and producer evaluations the rows share).  Every load is issued
+// before any store (outputs are kept in registers), so the loads overlap.
+template <PointFn F, int NO, int KC, int UJ>
 __global__ void __launch_bounds__(SU_BX * SU_BY) suite_kernel(const __grid_constant__ SuiteArgs a) {
     const int i = a.d.lo[0] + blockIdx.x * SU_BX + threadIdx.x;
-    const int j = a.d.lo[1] + blockIdx.y * SU_BY + threadIdx.y;
+    const int j = a.d.lo[1] + (blockIdx.y * SU_BY + threadIdx.y) * UJ;
     const int k0 = a.d.lo[2] + blockIdx.z * KC;
     griddep_wait();  // PDL: inputs may be the previous kernel's outputs
     if (i >= a.d.hi[0] || j >= a.d.hi[1]) {
         griddep_launch_dependents();
         return;
     }
-    double r[KC][NO];
-#pragma unroll
-    for (int kk = 0; kk < KC; ++kk) F(a.in, a.sc, i, j, min(k0 + kk, a.d.hi[2] - 1), r[kk]);
+    double r[KC][UJ][NO];
 #pragma unroll
     for (int kk = 0; kk < KC; ++kk)
-        if (k0 + kk < a.d.hi[2]) {
 #pragma unroll
-            for (int o = 0; o < NO; ++o) a.out[o].p[i + j * a.out[o].sj + (k0 + kk) * a.out[o].sk] = r[kk][o];
-        }
+        for (int u = 0; u < UJ; ++u) F(a.in, a.sc, i, min(j + u, a.d.hi[1] - 1), min(k0 + kk, a.d.hi[2] - 1), r[kk][u]);
+#pragma unroll
+    for (int kk = 0; kk < KC; ++kk)
+#pragma unroll
+        for (int u = 0; u < UJ; ++u)
+            if (k0 + kk < a.d.hi[2] && j + u < a.d.hi[1]) {
+#pragma unroll
+                for (int o = 0; o < NO; ++o)
+                    a.out[o].p[i + (j + u) * a.out[o].sj + (k0 + kk) * a.out[o].sk] = r[kk][u][o];
+            }
     griddep_launch_dependents();  // late: dependents launched early would idle in griddepcontrol.wait
+}
+
+template <int UJ>
+cudaError_t launch_suite_u(int program_id, const SuiteArgs &a, cudaStream_t s) {
+    constexpr int KC = SU_KC;
+    const Dom &d = a.d;
+    dim3 block(SU_BX, SU_BY, 1);
+    dim3 grid((d.hi[0] - d.lo[0] + SU_BX - 1) / SU_BX, (d.hi[1] - d.lo[1] + SU_BY * UJ - 1) / (SU_BY * UJ),
+              (d.hi[2] - d.lo[2] + KC - 1) / KC);
+    switch (program_id) {
+    case OEC_PROG_UVBKE: return launch_pdl(suite_kernel<uvbke_pt, 2, KC, UJ>, grid, block, 0, s, a);
+    case OEC_PROG_P_GRAD_C: return launch_pdl(suite_kernel<p_grad_c_pt, 2, KC, UJ>, grid, block, 0, s, a);
+    case OEC_PROG_NH_P_GRAD: return launch_pdl(suite_kernel<nh_p_grad_pt, 2, KC, UJ>, grid, block, 0, s, a);
+    case OEC_PROG_FVTP2D_QI: return launch_pdl(suite_kernel<fvtp2d_qi_pt, 2, KC, UJ>, grid, block, 0, s, a);
+    case OEC_PROG_FVTP2D_QJ: return launch_pdl(suite_kernel<fvtp2d_qj_pt, 3, KC, UJ>, grid, block, 0, s, a);
+    case OEC_PROG_FVTP2D_FLUX: return launch_pdl(suite_kernel<fvtp2d_flux_pt, 2, KC, UJ>, grid, block, 0, s, a);
+    case OEC_PROG_FASTWAVES: return launch_pdl(suite_kernel<fastwaves_pt, 2, KC, UJ>, grid, block, 0, s, a);
+    default: return cudaErrorInvalidValue;
+    }
 }
 
 }  // namespace
 
 cudaError_t launch_suite(int program_id, const FV *in, const FO *out, const double *scalars, const Dom &d,
-                         cudaStream_t s, int *launches) {
+                         int unroll, cudaStream_t s, int *launches) {
     SuiteArgs a;
     for (int q = 0; q < 9; ++q) a.in[q] = in[q];
     for (int q = 0; q < 3; ++q) a.out[q] = out[q];
     a.sc[0] = scalars[0];
     a.sc[1] = scalars[1];
     a.d = d;
-    constexpr int KC = SU_KC;
-    dim3 block(SU_BX, SU_BY, 1);
-    dim3 grid((d.hi[0] - d.lo[0] + SU_BX - 1) / SU_BX, (d.hi[1] - d.lo[1] + SU_BY - 1) / SU_BY,
-              (d.hi[2] - d.lo[2] + KC - 1) / KC);
-    cudaError_t e = cudaSuccess;
-    switch (program_id) {
-    case OEC_PROG_UVBKE: e = launch_pdl(suite_kernel<uvbke_pt, 2, KC>, grid, block, 0, s, a); break;
-    case OEC_PROG_P_GRAD_C: e = launch_pdl(suite_kernel<p_grad_c_pt, 2, KC>, grid, block, 0, s, a); break;
-    case OEC_PROG_NH_P_GRAD: e = launch_pdl(suite_kernel<nh_p_grad_pt, 2, KC>, grid, block, 0, s, a); break;
-    case OEC_PROG_FVTP2D_QI: e = launch_pdl(suite_kernel<fvtp2d_qi_pt, 2, KC>, grid, block, 0, s, a); break;
-    case OEC_PROG_FVTP2D_QJ: e = launch_pdl(suite_kernel<fvtp2d_qj_pt, 3, KC>, grid, block, 0, s, a); break;
-    case OEC_PROG_FVTP2D_FLUX: e = launch_pdl(suite_kernel<fvtp2d_flux_pt, 2, KC>, grid, block, 0, s, a); break;
-    case OEC_PROG_FASTWAVES: e = launch_pdl(suite_kernel<fastwaves_pt, 2, KC>, grid, block, 0, s, a); break;
-    default: return cudaErrorInvalidValue;
-    }
+    cudaError_t e = unroll == 4 ? launch_suite_u<4>(program_id, a, s)
+                  : unroll == 2 ? launch_suite_u<2>(program_id, a, s)
+                                : launch_suite_u<1>(program_id, a, s);
     ++*launches;
     return e != cudaSuccess ? e : cudaGetLastError();
 }

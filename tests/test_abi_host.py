@@ -111,15 +111,15 @@ def test_error_arg_counts_and_program():
     assert _status(lambda: oec.oec_apply_program("hdiff", [inp, cf], [out], dom_ub=(8, 8, 2), variant=5))[0] == 1
 
 
-def test_unfused_variant_only_for_hdiff_vadv():
+def test_unroll_variant_rejected_for_vadv():
     dom = (4, 4, 2)
-    uc = _host((2, 5, 4), (0, -1, 0), (4, 4, 2))
-    vc = _host((2, 4, 5), (-1, 0, 0), (4, 4, 2))
-    ca = oec.oec_field_wrap(np.zeros((1, 4, 4)), (0, 0, 0), (4, 4, 1), k_invariant=True)
-    rs = oec.oec_field_wrap(np.zeros((1, 4, 4)), (0, 0, 0), (4, 4, 1), k_invariant=True)
-    ub, vb = _host((2, 4, 4), (0, 0, 0), dom), _host((2, 4, 4), (0, 0, 0), dom)
-    stt, _ = _status(lambda: oec.oec_apply_program("uvbke", [uc, vc, ca, rs], [ub, vb], dom_ub=dom, variant=1))
-    assert stt == 7
+    f = [_host((2, 4, 4), (0, 0, 0), dom) for _ in range(4)]
+    w = _host((2, 4, 5), (0, 0, 0), (5, 4, 2))
+    o = _host((2, 4, 4), (0, 0, 0), dom)
+    for variant in (3, 4):
+        stt, msg = _status(lambda: oec.oec_apply_program("vadv", [f[0], w, f[1], f[2], f[3]], [o], dom_ub=dom,
+                                                         variant=variant))
+        assert stt == 7 and "unroll" in msg
 
 
 def test_error_layout_stride0():

@@ -236,13 +236,37 @@ def test_vadv_odd_pitch_register_kernel():
     _assert_parity(t_out.cpu().numpy(), r["utens_stage_out"], "vadv odd pitch")
 
 
-@pytest.mark.parametrize("program", ["hdiff", "vadv"])
+@pytest.mark.parametrize("program", synth.ALL_PROGRAMS)
 @pytest.mark.parametrize("domain", [(33, 31, 5), (128, 128, 80)])
 def test_unfused_original_level(program, domain):
     # OEC_VARIANT_UNFUSED: the paper's "original" level (one kernel per operator, temporaries in HBM)
     # computes the same values bit for bit
     _check(program, domain, seed=2, variant=1)
     _check(program, domain, seed=2, variant=1, dom_lb=(1, 2, 0), dom_ub=(domain[0] - 3, domain[1] - 1, domain[2]))
+
+
+HORIZONTAL = [p for p in synth.ALL_PROGRAMS if p != "vadv"]
+
+
+@pytest.mark.parametrize("program", HORIZONTAL)
+@pytest.mark.parametrize("variant", [2, 3, 4])  # inline, inline+unroll(2), inline+unroll(4)
+@pytest.mark.parametrize("domain", [(37, 29, 3), (64, 18, 2), (5, 3, 1)])
+def test_inline_and_unrolled_levels(program, variant, domain):
+    # row counts not divisible by the 4 x unroll rows of a block: ragged j tail on every level
+    _check(program, domain, seed=3, variant=variant)
+    _check(program, domain, seed=3, variant=variant, order=(0, 1, 2), out_halo=(1, 2, 0))
+    if domain[1] > 4:
+        _check(program, domain, seed=3, variant=variant, dom_lb=(0, 1, 0), dom_ub=(domain[0] - 1, domain[1] - 2, domain[2]))
+
+
+def test_vadv_inline_level_and_unroll_rejected():
+    from paper_2005_13014_b200 import oec
+
+    _check("vadv", (45, 7, 20), seed=3, variant=2)  # one thread per column (register/smem kernel)
+    host = synth.make_inputs("vadv", (8, 4, 3), seed=0)
+    with pytest.raises(oec.OecError) as ei:
+        run_gpu("vadv", host, (8, 4, 3), variant=3)
+    assert ei.value.status == 7
 
 
 def test_hdiff_large_config_ragged():
