@@ -3,7 +3,9 @@
 Written from the same definitions as oracle/oec_oracle.c (readings R1-R11) but with
 whole-array slicing instead of point loops, so a slip in either (an index, a sign, an operand
 order) shows up as a mismatch.  numpy elementwise fp64 arithmetic is IEEE RNE without
-contraction, so the two agree bitwise.
+contraction, so the two agree bitwise.  float32 fields give the binary32 instance:
+numpy keeps float32 arithmetic in float32 and rounds Python-float constants to float32 (NEP 50),
+as the C oracle's R() does.
 """
 from __future__ import annotations
 
@@ -85,7 +87,7 @@ def vadv(f, dtr: float, lo, hi) -> np.ndarray:
         r = 1.0 / (b[q] - cp[q - 1] * a[q])
         cp[q] = c[q] * r
         dp[q] = (d[q] - dp[q - 1] * a[q]) * r
-    out = np.empty((K, j1 - j0, i1 - i0))
+    out = np.empty((K, j1 - j0, i1 - i0), dtype=dp[0].dtype)
     x = dp[K - 1]
     out[K - 1] = dtr * (x - F("u_pos", k0 + K - 1))
     for q in range(K - 2, -1, -1):

@@ -13,7 +13,7 @@
  * inlined per-point expression (stencil inlining): it clones producer expression trees
  * and never reassociates, so both variants must agree bitwise (tests pin that).
  *
- * Arithmetic: IEEE fp64, round-to-nearest-even, NO contraction (built with -O2 -fno-fast-math
+ * Arithmetic: IEEE fp64 (the f32 instance: binary32), round-to-nearest-even, NO contraction (built with -O2 -fno-fast-math
  * -ffp-contract=off).  Sums are evaluated exactly in the parenthesised order
  * written below (readings R3, R10).  Out-of-range reads are detected and make the
  * call return ORACLE_ERR_RANGE ("out-of-range access traps").
@@ -49,10 +49,23 @@
 #define ORACLE_ERR_RANGE 2
 #define ORACLE_ERR_ARG 1
 
+/* Precision ("single-precision (f32) and double-precision (f64)"): compiled twice, once
+ * with real = double (entry points oracle_*) and once with -DORACLE_F32, real = float (entry
+ * points oracle_*_f32).  Every constant is rounded to `real` (R()), so an f32 expression is
+ * evaluated entirely in IEEE binary32 (FLT_EVAL_METHOD 0 on x86-64), as written. */
+#ifdef ORACLE_F32
+typedef float real;
+#define SFX(name) name##_f32
+#else
+typedef double real;
+#define SFX(name) name
+#endif
+#define R(x) ((real)(x))
+
 /* A dense host field over its allocated range [lb, ub), index order [k][j][i] (i fastest).
  * A k-invariant (2D) field has lb[2] = 0, ub[2] = 1 and ignores k. */
 typedef struct {
-    double *d;
+    real *d;
     int64_t lb[3];
     int64_t ub[3];
     int32_t k_invariant;
@@ -60,11 +73,11 @@ typedef struct {
 
 static int g_range_error; /* set when any access falls outside a field's allocation */
 
-static double *at(const ofield *f, int64_t i, int64_t j, int64_t k) {
+static real *at(const ofield *f, int64_t i, int64_t j, int64_t k) {
     if (f->k_invariant) k = 0;
     if (i < f->lb[0] || i >= f->ub[0] || j < f->lb[1] || j >= f->ub[1] || k < f->lb[2] || k >= f->ub[2]) {
         g_range_error = 1;
-        static double trap = NAN;
+        static real trap = NAN;
         return &trap;
     }
     int64_t ni = f->ub[0] - f->lb[0], nj = f->ub[1] - f->lb[1];
@@ -81,7 +94,7 @@ static ofield temp_field(const int64_t lb[3], const int64_t ub[3]) {
         n *= (ub[d] - lb[d]) > 0 ? (ub[d] - lb[d]) : 0;
     }
     t.k_invariant = 0;
-    t.d = (double *)malloc((size_t)(n > 0 ? n : 1) * sizeof(double));
+    t.d = (real *)malloc((size_t)(n > 0 ? n : 1) * sizeof(real));
     for (int64_t q = 0; q < n; ++q) t.d[q] = NAN;
     return t;
 }
@@ -94,6 +107,7 @@ static void set_threads(int nthreads) {
 #endif
 }
 
+#ifndef ORACLE_F32
 int oracle_max_threads(void) {
 #ifdef _OPENMP
     return omp_get_max_threads();
@@ -101,6 +115,7 @@ int oracle_max_threads(void) {
     return 1;
 #endif
 }
+#endif
 
 /* ------------------------------------------------------------------------------------------ */
 /* hdiff                                                                                      */
@@ -108,11 +123,11 @@ int oracle_max_threads(void) {
 
 /* The flux limiter (reading R4): strict '>' -- a product of exactly 0 keeps the flux; a NaN
  * product compares false and keeps the flux. */
-static double limit(double f, double din) { return (f * din > 0.0) ? 0.0 : f; }
+static real limit(real f, real din) { return (f * din > R(0.0)) ? R(0.0) : f; }
 
-static double lap_at(const ofield *in, int64_t i, int64_t j, int64_t k) {
+static real lap_at(const ofield *in, int64_t i, int64_t j, int64_t k) {
     return ((A(in, i - 1, j, k) + A(in, i + 1, j, k)) + (A(in, i, j - 1, k) + A(in, i, j + 1, k))) -
-           4.0 * A(in, i, j, k);
+           R(4.0) * A(in, i, j, k);
 }
 
 /* limiter_on = 0 is the debug "limiter off" variant used only by the biharmonic pin. */
@@ -130,12 +145,12 @@ static int hdiff_unfused(const ofield *in, const ofield *coeff, ofield *out, con
             for (int64_t i = llo[0]; i < lhi[0]; ++i) A(&lap, i, j, k) = lap_at(in, i, j, k);
         for (int64_t j = xlo[1]; j < xhi[1]; ++j)
             for (int64_t i = xlo[0]; i < xhi[0]; ++i) {
-                double f = A(&lap, i + 1, j, k) - A(&lap, i, j, k);
+                real f = A(&lap, i + 1, j, k) - A(&lap, i, j, k);
                 A(&flx, i, j, k) = limiter_on ? limit(f, A(in, i + 1, j, k) - A(in, i, j, k)) : f;
             }
         for (int64_t j = ylo[1]; j < yhi[1]; ++j)
             for (int64_t i = ylo[0]; i < yhi[0]; ++i) {
-                double g = A(&lap, i, j + 1, k) - A(&lap, i, j, k);
+                real g = A(&lap, i, j + 1, k) - A(&lap, i, j, k);
                 A(&fly, i, j, k) = limiter_on ? limit(g, A(in, i, j + 1, k) - A(in, i, j, k)) : g;
             }
         for (int64_t j = lo[1]; j < hi[1]; ++j)
@@ -150,12 +165,12 @@ static int hdiff_unfused(const ofield *in, const ofield *coeff, ofield *out, con
 }
 
 /* Fused: the inlined per-point expression, producer trees cloned at every offset. */
-static double flx_at(const ofield *in, int64_t i, int64_t j, int64_t k) {
-    double f = lap_at(in, i + 1, j, k) - lap_at(in, i, j, k);
+static real flx_at(const ofield *in, int64_t i, int64_t j, int64_t k) {
+    real f = lap_at(in, i + 1, j, k) - lap_at(in, i, j, k);
     return limit(f, A(in, i + 1, j, k) - A(in, i, j, k));
 }
-static double fly_at(const ofield *in, int64_t i, int64_t j, int64_t k) {
-    double g = lap_at(in, i, j + 1, k) - lap_at(in, i, j, k);
+static real fly_at(const ofield *in, int64_t i, int64_t j, int64_t k) {
+    real g = lap_at(in, i, j + 1, k) - lap_at(in, i, j, k);
     return limit(g, A(in, i, j + 1, k) - A(in, i, j, k));
 }
 
@@ -178,7 +193,7 @@ static int hdiff_fused(const ofield *in, const ofield *coeff, ofield *out, const
 
 /* variant: 0 = unfused ("original"), 1 = fused (inlined), 2 = fused with reversed loop order,
  * 3 = unfused with the limiter switched off (debug variant for the biharmonic pin only). */
-int oracle_hdiff(const ofield *in, const ofield *coeff, ofield *out, const int64_t lo[3], const int64_t hi[3],
+int SFX(oracle_hdiff)(const ofield *in, const ofield *coeff, ofield *out, const int64_t lo[3], const int64_t hi[3],
                  int variant, int nthreads) {
     if (!in || !coeff || !out || !lo || !hi) return ORACLE_ERR_ARG;
     set_threads(nthreads);
@@ -197,34 +212,34 @@ int oracle_hdiff(const ofield *in, const ofield *coeff, ofield *out, const int64
 /* vadv                                                                                       */
 /* ------------------------------------------------------------------------------------------ */
 
-#define BET_M 0.5
-#define BET_P 0.5
+#define BET_M R(0.5)
+#define BET_P R(0.5)
 
 /* Tridiagonal coefficients (a, b, c, d) of level k of column (i,j); k0 = top, kN = bottom
  * level of the domain (reading R8: the k = k0 / k = kN branches are the boundary rows). */
 static void vadv_coeffs(const ofield *u_stage, const ofield *wcon, const ofield *u_pos, const ofield *utens,
-                        const ofield *utens_stage_in, double dtr, int64_t i, int64_t j, int64_t k, int64_t k0,
-                        int64_t kN, double *a, double *b, double *c, double *d) {
-    double corr;
+                        const ofield *utens_stage_in, real dtr, int64_t i, int64_t j, int64_t k, int64_t k0,
+                        int64_t kN, real *a, real *b, real *c, real *d) {
+    real corr;
     if (k == k0) {
-        double gcv = 0.25 * (A(wcon, i + 1, j, k + 1) + A(wcon, i, j, k + 1));
-        double cs = gcv * BET_M;
-        *a = 0.0;
+        real gcv = R(0.25) * (A(wcon, i + 1, j, k + 1) + A(wcon, i, j, k + 1));
+        real cs = gcv * BET_M;
+        *a = R(0.0);
         *c = gcv * BET_P;
         *b = dtr - *c;
         corr = -cs * (A(u_stage, i, j, k + 1) - A(u_stage, i, j, k));
     } else if (k == kN) {
-        double gav = -0.25 * (A(wcon, i + 1, j, k) + A(wcon, i, j, k));
-        double as = gav * BET_M;
+        real gav = R(-0.25) * (A(wcon, i + 1, j, k) + A(wcon, i, j, k));
+        real as = gav * BET_M;
         *a = gav * BET_P;
-        *c = 0.0;
+        *c = R(0.0);
         *b = dtr - *a;
         corr = -as * (A(u_stage, i, j, k - 1) - A(u_stage, i, j, k));
     } else {
-        double gav = -0.25 * (A(wcon, i + 1, j, k) + A(wcon, i, j, k));
-        double gcv = 0.25 * (A(wcon, i + 1, j, k + 1) + A(wcon, i, j, k + 1));
-        double as = gav * BET_M;
-        double cs = gcv * BET_M;
+        real gav = R(-0.25) * (A(wcon, i + 1, j, k) + A(wcon, i, j, k));
+        real gcv = R(0.25) * (A(wcon, i + 1, j, k + 1) + A(wcon, i, j, k + 1));
+        real as = gav * BET_M;
+        real cs = gcv * BET_M;
         *a = gav * BET_P;
         *c = gcv * BET_P;
         *b = (dtr - *a) - *c;
@@ -237,7 +252,7 @@ static void vadv_coeffs(const ofield *u_stage, const ofield *wcon, const ofield 
  * materialises c', d'; the backward sweep materialises x; the output stencil writes
  * utens_stage_out = dtr*(x - u_pos). */
 static int vadv_unfused(const ofield *u_stage, const ofield *wcon, const ofield *u_pos, const ofield *utens,
-                        const ofield *utens_stage_in, ofield *out, double dtr, const int64_t lo[3], const int64_t hi[3]) {
+                        const ofield *utens_stage_in, ofield *out, real dtr, const int64_t lo[3], const int64_t hi[3]) {
     ofield fa = temp_field(lo, hi), fb = temp_field(lo, hi), fc = temp_field(lo, hi), fd = temp_field(lo, hi);
     ofield cp = temp_field(lo, hi), dp = temp_field(lo, hi), x = temp_field(lo, hi);
     int64_t k0 = lo[2], kN = hi[2] - 1;
@@ -249,13 +264,13 @@ static int vadv_unfused(const ofield *u_stage, const ofield *wcon, const ofield 
                             &A(&fb, i, j, k), &A(&fc, i, j, k), &A(&fd, i, j, k));
         /* forward sweep (Thomas elimination): reciprocal, then multiply (reading R10) */
         for (int64_t i = lo[0]; i < hi[0]; ++i) {
-            double r = 1.0 / A(&fb, i, j, k0);
+            real r = R(1.0) / A(&fb, i, j, k0);
             A(&cp, i, j, k0) = A(&fc, i, j, k0) * r;
             A(&dp, i, j, k0) = A(&fd, i, j, k0) * r;
         }
         for (int64_t k = k0 + 1; k <= kN; ++k)
             for (int64_t i = lo[0]; i < hi[0]; ++i) {
-                double r = 1.0 / (A(&fb, i, j, k) - A(&cp, i, j, k - 1) * A(&fa, i, j, k));
+                real r = R(1.0) / (A(&fb, i, j, k) - A(&cp, i, j, k - 1) * A(&fa, i, j, k));
                 A(&cp, i, j, k) = A(&fc, i, j, k) * r;
                 A(&dp, i, j, k) = (A(&fd, i, j, k) - A(&dp, i, j, k - 1) * A(&fa, i, j, k)) * r;
             }
@@ -274,32 +289,32 @@ static int vadv_unfused(const ofield *u_stage, const ofield *wcon, const ofield 
 
 /* Fused: one pass per column, c' and d' in a per-column scratch (never a global temporary). */
 static int vadv_fused(const ofield *u_stage, const ofield *wcon, const ofield *u_pos, const ofield *utens,
-                      const ofield *utens_stage_in, ofield *out, double dtr, const int64_t lo[3], const int64_t hi[3],
+                      const ofield *utens_stage_in, ofield *out, real dtr, const int64_t lo[3], const int64_t hi[3],
                       int reverse) {
     int64_t k0 = lo[2], kN = hi[2] - 1, K = hi[2] - lo[2];
 #pragma omp parallel
     {
-        double *cp = (double *)malloc((size_t)K * sizeof(double));
-        double *dp = (double *)malloc((size_t)K * sizeof(double));
+        real *cp = (real *)malloc((size_t)K * sizeof(real));
+        real *dp = (real *)malloc((size_t)K * sizeof(real));
 #pragma omp for schedule(static)
         for (int64_t jj = lo[1]; jj < hi[1]; ++jj) {
             int64_t j = reverse ? (hi[1] - 1 - (jj - lo[1])) : jj;
             for (int64_t ii = lo[0]; ii < hi[0]; ++ii) {
                 int64_t i = reverse ? (hi[0] - 1 - (ii - lo[0])) : ii;
                 for (int64_t k = k0; k <= kN; ++k) {
-                    double a, b, c, d;
+                    real a, b, c, d;
                     vadv_coeffs(u_stage, wcon, u_pos, utens, utens_stage_in, dtr, i, j, k, k0, kN, &a, &b, &c, &d);
                     if (k == k0) {
-                        double r = 1.0 / b;
+                        real r = R(1.0) / b;
                         cp[0] = c * r;
                         dp[0] = d * r;
                     } else {
-                        double r = 1.0 / (b - cp[k - k0 - 1] * a);
+                        real r = R(1.0) / (b - cp[k - k0 - 1] * a);
                         cp[k - k0] = c * r;
                         dp[k - k0] = (d - dp[k - k0 - 1] * a) * r;
                     }
                 }
-                double x = dp[K - 1];
+                real x = dp[K - 1];
                 A(out, i, j, kN) = dtr * (x - A(u_pos, i, j, kN));
                 for (int64_t k = kN - 1; k >= k0; --k) {
                     x = dp[k - k0] - cp[k - k0] * x;
@@ -314,7 +329,7 @@ static int vadv_fused(const ofield *u_stage, const ofield *wcon, const ofield *u
 }
 
 /* variant: 0 = unfused, 1 = fused, 2 = fused with reversed column order. K >= 2 required. */
-int oracle_vadv(const ofield *u_stage, const ofield *wcon, const ofield *u_pos, const ofield *utens,
+int SFX(oracle_vadv)(const ofield *u_stage, const ofield *wcon, const ofield *u_pos, const ofield *utens,
                 const ofield *utens_stage_in, ofield *out, double dtr_stage, const int64_t lo[3], const int64_t hi[3],
                 int variant, int nthreads) {
     if (!u_stage || !wcon || !u_pos || !utens || !utens_stage_in || !out || !lo || !hi) return ORACLE_ERR_ARG;
@@ -322,22 +337,22 @@ int oracle_vadv(const ofield *u_stage, const ofield *wcon, const ofield *u_pos, 
     set_threads(nthreads);
     g_range_error = 0;
     switch (variant) {
-    case 0: vadv_unfused(u_stage, wcon, u_pos, utens, utens_stage_in, out, dtr_stage, lo, hi); break;
-    case 1: vadv_fused(u_stage, wcon, u_pos, utens, utens_stage_in, out, dtr_stage, lo, hi, 0); break;
-    case 2: vadv_fused(u_stage, wcon, u_pos, utens, utens_stage_in, out, dtr_stage, lo, hi, 1); break;
+    case 0: vadv_unfused(u_stage, wcon, u_pos, utens, utens_stage_in, out, R(dtr_stage), lo, hi); break;
+    case 1: vadv_fused(u_stage, wcon, u_pos, utens, utens_stage_in, out, R(dtr_stage), lo, hi, 0); break;
+    case 2: vadv_fused(u_stage, wcon, u_pos, utens, utens_stage_in, out, R(dtr_stage), lo, hi, 1); break;
     default: return ORACLE_ERR_ARG;
     }
     return g_range_error ? ORACLE_ERR_RANGE : ORACLE_OK;
 }
 
 /* Exposed for the dense-solve pin: the (a, b, c, d) rows of one column, k = lo2 .. hi2-1. */
-int oracle_vadv_system(const ofield *u_stage, const ofield *wcon, const ofield *u_pos, const ofield *utens,
+int SFX(oracle_vadv_system)(const ofield *u_stage, const ofield *wcon, const ofield *u_pos, const ofield *utens,
                        const ofield *utens_stage_in, double dtr_stage, int64_t i, int64_t j, int64_t k_lo,
-                       int64_t k_hi, double *a, double *b, double *c, double *d) {
+                       int64_t k_hi, real *a, real *b, real *c, real *d) {
     if (k_hi - k_lo < 2) return ORACLE_ERR_ARG;
     g_range_error = 0;
     for (int64_t k = k_lo; k < k_hi; ++k)
-        vadv_coeffs(u_stage, wcon, u_pos, utens, utens_stage_in, dtr_stage, i, j, k, k_lo, k_hi - 1, &a[k - k_lo],
+        vadv_coeffs(u_stage, wcon, u_pos, utens, utens_stage_in, R(dtr_stage), i, j, k, k_lo, k_hi - 1, &a[k - k_lo],
                     &b[k - k_lo], &c[k - k_lo], &d[k - k_lo]);
     return g_range_error ? ORACLE_ERR_RANGE : ORACLE_OK;
 }

@@ -119,8 +119,19 @@ def _where(c, x, y):
     return np.where(c, x, y)
 
 
+def _dtype(fields, names):
+    dts = {fields[n].data.dtype for n in names}
+    assert len(dts) == 1 and dts <= {np.dtype(np.float64), np.dtype(np.float32)}, dts
+    return dts.pop()
+
+
 def run_unfused(prog: Program, fields: Dict[str, HostField], scalars: Dict[str, float], domain_lo, domain_hi,
                 outputs: Optional[Dict[str, HostField]] = None) -> Dict[str, HostField]:
+    # precision = the inputs' dtype (float64, or float32 for the paper's f32 runs): scalars
+    # are rounded to it and numpy keeps float32 expressions in float32 (Python-float constants
+    # are rounded to float32, NEP 50)
+    dt = _dtype(fields, prog.inputs)
+    scalars = {k: dt.type(v) for k, v in scalars.items()}
     env: Dict[str, HostField] = {n: fields[n] for n in prog.inputs}
     # universe: the bounding box of all input allocations (k-invariant fields: all k)
     ulo = [min(f.lb[d] for f in env.values() if not (d == 2 and f.k_invariant)) for d in range(3)]
@@ -148,7 +159,9 @@ def run_unfused(prog: Program, fields: Dict[str, HostField], scalars: Dict[str, 
         with np.errstate(all="ignore"):
             vals = _as_tuple(ap.fn(a, scalars, _where), len(ap.results))
         for rname, v in zip(ap.results, vals):
-            arr = np.ascontiguousarray(np.broadcast_to(np.asarray(v, dtype=np.float64), shape))
+            v = np.asarray(v)
+            assert v.dtype == dt, (prog.name, rname, v.dtype)  # no silent promotion
+            arr = np.ascontiguousarray(np.broadcast_to(v, shape))
             env[rname] = HostField(arr, tuple(lo), tuple(hi))
     res = outputs if outputs is not None else {}
     for oname, tname in prog.outputs:
@@ -183,8 +196,9 @@ def run_fused(prog: Program, fields: Dict[str, HostField], scalars: Dict[str, fl
         for r_idx, r in enumerate(ap.results):
             producer[r] = (ap, r_idx)
     touched: Dict[str, Set[Tuple[int, int, int]]] = {n: set() for n in prog.inputs}
-    memo: Dict[Tuple[str, int, int, int], np.float64] = {}
-    sc = {k: np.float64(v) for k, v in scalars.items()}
+    dt = _dtype(fields, prog.inputs)
+    memo: Dict[Tuple[str, int, int, int], np.floating] = {}
+    sc = {k: dt.type(v) for k, v in scalars.items()}
 
     def value(name, i, j, k):
         if name in fields and name in touched:
@@ -201,9 +215,10 @@ def run_fused(prog: Program, fields: Dict[str, HostField], scalars: Dict[str, fl
             def a(n, di=0, dj=0, dk=0):
                 return value(n, i + di, j + dj, k + dk)
 
-            vals = _as_tuple(ap.fn(a, sc, lambda c, x, y: x if c else y), len(ap.results))
+            vals = _as_tuple(ap.fn(a, sc, lambda c, x, y: dt.type(x if c else y)), len(ap.results))
             for r, v in zip(ap.results, vals):
-                memo[(r, i, j, k)] = np.float64(v)
+                assert np.asarray(v).dtype == dt, (prog.name, r)  # no silent promotion
+                memo[(r, i, j, k)] = v
         return memo[key]
 
     if points is None:

@@ -28,7 +28,7 @@ Int3 = Tuple[int, int, int]
 class HostField:
     """Dense host array over [lb, ub) (absolute coords, origin = domain lower bound)."""
 
-    data: np.ndarray  # float64, shape (ub2-lb2, ub1-lb1, ub0-lb0) -> [k][j][i]
+    data: np.ndarray  # float64 (or float32), shape (ub2-lb2, ub1-lb1, ub0-lb0) -> [k][j][i]
     lb: Int3
     ub: Int3
     k_invariant: bool = False
@@ -228,12 +228,14 @@ def _draw(rng: np.random.Generator, dist: str, shape, lb_k: int) -> np.ndarray:
     raise ValueError(f"unknown distribution {dist!r}")
 
 
-def make_inputs(program: str, domain: Int3, seed: int = 0, smooth: bool = False) -> Dict[str, HostField]:
+def make_inputs(program: str, domain: Int3, seed: int = 0, smooth: bool = False,
+                dtype=np.float64) -> Dict[str, HostField]:
     """Seeded inputs of `program` on `domain` = (Ni, Nj, Nk).
 
     Fields are drawn in the fixed order of PROGRAMS[program].inputs from one PCG64(seed)
     stream over their entire allocation.  `smooth` (hdiff only) replaces `in` by the smooth
     field of SURVEY §8(d): sin(2 pi i/Ni) cos(2 pi j/Nj) (1 + k/Nk) + 0.01 U[-1,1].
+    dtype=np.float32 draws the same fp64 values and rounds them to binary32 (P:556 f32 runs).
     """
     spec = PROGRAMS[program]
     rng = np.random.Generator(np.random.PCG64(seed))
@@ -250,19 +252,24 @@ def make_inputs(program: str, domain: Int3, seed: int = 0, smooth: bool = False)
                 np.sin(2 * np.pi * ii / domain[0]) * np.cos(2 * np.pi * jj / domain[1]) * (1.0 + kk / domain[2])
                 + 0.01 * data
             )
-        out[s.name] = HostField(np.ascontiguousarray(data, dtype=np.float64), lb, ub, s.k_invariant)
+        out[s.name] = HostField(np.ascontiguousarray(data, dtype=np.float64).astype(dtype), lb, ub, s.k_invariant)
     return out
+
+
+def as_dtype(fields: Dict[str, HostField], dtype) -> Dict[str, HostField]:
+    """The same fields converted to `dtype` (float32 -> float64 is exact)."""
+    return {n: HostField(np.ascontiguousarray(f.data.astype(dtype)), f.lb, f.ub, f.k_invariant) for n, f in fields.items()}
 
 
 def scalars(program: str) -> Dict[str, float]:
     return dict(PROGRAMS[program].scalars)
 
 
-def empty_outputs(program: str, domain: Int3, fill: float = np.nan) -> Dict[str, HostField]:
+def empty_outputs(program: str, domain: Int3, fill: float = np.nan, dtype=np.float64) -> Dict[str, HostField]:
     """Output fields allocated exactly on the domain, pre-filled with `fill` (sentinel)."""
     res = {}
     for name in PROGRAMS[program].outputs:
-        res[name] = HostField(np.full((domain[2], domain[1], domain[0]), fill), (0, 0, 0), tuple(domain))
+        res[name] = HostField(np.full((domain[2], domain[1], domain[0]), fill, dtype=dtype), (0, 0, 0), tuple(domain))
     return res
 
 
@@ -281,6 +288,7 @@ __all__ = [
     "ALL_PROGRAMS",
     "alloc_range",
     "make_inputs",
+    "as_dtype",
     "scalars",
     "empty_outputs",
     "probe_field",
