@@ -434,10 +434,11 @@ def main():
         e2e = e2e_measure(oec, torch, hh, vh, dtr, domain, args.e2e_steps, world)
 
     # ---- remaining suite (evidence for SURVEY §8(a) a7; not part of the step) ----
-    suite_res = levels = None
+    suite_res = levels = f32_res = None
     if not args.no_suite and world == 1:
         suite_res = suite_measure(oec, torch, domain, l2, peak)
         levels = levels_measure(oec, torch, domain, l2, peak)
+        f32_res = f32_measure(oec, torch, domain, l2, peak)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -467,6 +468,8 @@ def main():
             res["suite"] = suite_res
         if levels is not None:
             res["optimization_levels"] = levels
+        if f32_res is not None:
+            res["f32"] = f32_res
         print(json.dumps(res), flush=True)
     if decomp:
         dist.barrier()
@@ -511,19 +514,20 @@ def e2e_measure(oec, torch, hh, vh, dtr, domain, steps, world):
             "path": "oec_hdiff/oec_vadv with OEC_DEVICE_HOST fields (pinned), staged by liboec, synchronous"}
 
 
-def program_measure(oec, torch, program, domain, l2, peak, variant=0, reps=20):
-    """us per launch of one program (CUDA graph of R launches over R rotating input sets > 4x L2)."""
-    host = synth.make_inputs(program, domain, seed=0)
+def program_measure(oec, torch, program, domain, l2, peak, variant=0, reps=20, dtype=np.float64):
+    """us per launch of one program (CUDA graph of R launches over R rotating input sets > 4x L2).
+    dtype=np.float32: the paper's f32 runs; algorithmic bytes scale with the element size."""
+    host = synth.make_inputs(program, domain, seed=0, dtype=dtype)
     spec = synth.PROGRAMS[program]
     sc = [v for _, v in spec.scalars]
 
     def make():
         ins = [oec.field_from_host(host[s.name]) for s in spec.inputs]
-        outs = [oec.empty_like_domain(domain, fill=0.0) for _ in spec.outputs]
+        outs = [oec.empty_like_domain(domain, fill=0.0, dtype=dtype) for _ in spec.outputs]
         return ins, outs
 
     s0 = make()
-    set_bytes = sum(int(np.prod([f.ub[d] - f.lb[d] for d in range(3)])) * 8 for f in s0[0] + s0[1])
+    set_bytes = sum(int(np.prod([f.ub[d] - f.lb[d] for d in range(3)])) * f.itemsize for f in s0[0] + s0[1])
     R = max(2, math.ceil(4 * l2 / set_bytes) + 1)
     sets = [s0] + [make() for _ in range(R - 1)]
     for ins, outs in sets:  # also sizes any library workspace outside the capture
@@ -542,7 +546,7 @@ def program_measure(oec, torch, program, domain, l2, peak, variant=0, reps=20):
     b.record()
     torch.cuda.synchronize()
     us = 1e3 * a.elapsed_time(b) / (reps * R)
-    nbytes = program_bytes(program, domain)
+    nbytes = program_bytes(program, domain) * np.dtype(dtype).itemsize // 8
     del sets, s0, g
     return {"us_per_launch": us, "algorithmic_bytes": nbytes, "GB/s": nbytes / (us * 1e-6) / 1e9,
             "frac_of_hbm_peak": nbytes / (us * 1e-6) / 1e9 / peak,
@@ -551,6 +555,11 @@ def program_measure(oec, torch, program, domain, l2, peak, variant=0, reps=20):
 
 def suite_measure(oec, torch, domain, l2, peak):
     return {p: program_measure(oec, torch, p, domain, l2, peak) for p in synth.SUITE}
+
+
+def f32_measure(oec, torch, domain, l2, peak):
+    """Every program in binary32 (P:556 evaluates f32 and f64), default kernels."""
+    return {p: program_measure(oec, torch, p, domain, l2, peak, dtype=np.float32) for p in synth.ALL_PROGRAMS}
 
 
 def levels_measure(oec, torch, domain, l2, peak):

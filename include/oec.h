@@ -1,6 +1,7 @@
 /*
  * oec.h -- C ABI of liboec, the B200-native hot path of the Open Earth Compiler paper
- * (arXiv 2005.13014, "PAPER.md" below): fused fp64 stencil programs on 3D fields with halos.
+ * (arXiv 2005.13014, "PAPER.md" below): fused fp64 (and f32) stencil programs on 3D fields with
+ * halos.
  *
  * A STENCIL PROGRAM "loads the data from the input arrays, implements the stencil operators
  * inline, and stores the results to the output arrays" (§4.4).  Every entry
@@ -15,7 +16,7 @@
  *   computation domain the fields were made for ("The origin denotes the lower bound of the
  *   computation domain and has all coordinates set to zero", §4.2).  Ranges are
  *   [lb, ub): inclusive lower, exclusive upper bound.  i is the fastest dimension.
- * Fields.  An oec_field describes (does not own, unless `owned`) a strided fp64 array over its
+ * Fields.  An oec_field describes (does not own, unless `owned`) a strided fp64 or f32 array over its
  *   ALLOCATED range [lb, ub): element (i,j,k) lives at
  *     data + (i-lb[0])*stride[0] + (j-lb[1])*stride[1] + (k-lb[2])*stride[2]   (elements).
  *   stride[0] must be 1.  A k-invariant ("2D metric") field has lb[2] = 0, ub[2] = 1 and
@@ -37,8 +38,11 @@
  *   workspace on the current device: H2D copies of the inputs, the kernel, D2H copies of the
  *   outputs' domain, then it synchronises `stream` before returning (the end-to-end path).
  *   All fields of one call must be on the same side.
- * Numerics.  IEEE fp64, round-to-nearest-even, no contraction into FMA, expression order of the
- *   program definitions in DESIGN.md: results are bit-identical to the CPU oracle.
+ * Numerics.  IEEE fp64 -- or binary32 when the fields are OEC_F32 ("single-precision (f32) and
+ *   double-precision (f64)", §7.1) -- round-to-nearest-even, no contraction into FMA,
+ *   expression order of the program definitions in DESIGN.md: results are bit-identical to the
+ *   CPU oracle of the same precision.  All fields of one call share one dtype; scalars are
+ *   passed as double and rounded once to the fields' precision.
  * Errors.  Every call returns an oec_status; OEC_OK = 0.  No exception crosses the ABI.  The
  *   message of the last failing call on this thread is oec_last_error().  Launch failures are
  *   OEC_ERR_CUDA; asynchronous device faults surface at the caller's next synchronisation.
@@ -61,14 +65,15 @@ typedef enum {
     OEC_ERR_ARG = 1,         /* NULL pointer, bad enum, unknown program, wrong arg count     */
     OEC_ERR_SHAPE = 2,       /* allocation does not cover domain + extent, K < 2 (vadv), ... */
     OEC_ERR_ALIAS = 3,       /* an output overlaps an input or another output         */
-    OEC_ERR_DTYPE = 4,       /* dtype other than OEC_F64, or mixed devices                   */
+    OEC_ERR_DTYPE = 4,       /* unknown dtype, mixed dtypes, or mixed devices                */
     OEC_ERR_CUDA = 5,        /* CUDA runtime error (launch, allocation, copy)                */
     OEC_ERR_NCCL = 6,        /* NCCL error or NCCL not loadable                               */
     OEC_ERR_UNSUPPORTED = 7, /* valid request this build does not implement                  */
     OEC_ERR_LAYOUT = 8       /* stride[0] != 1, misaligned data, offsets overflow int32      */
 } oec_status;
 
-typedef enum { OEC_F64 = 0 } oec_dtype;
+/* Element types (P:556 evaluates every benchmark in both). */
+typedef enum { OEC_F64 = 0, OEC_F32 = 1 } oec_dtype;
 
 /* Kernel variants of oec_apply_program / oec_hdiff_variant: the paper's optimisation levels
    (§7.3: original, inline, inline+unroll(2), inline+unroll(4)) plus the tuned
@@ -111,13 +116,15 @@ const char *oec_last_error(void);
 /* Allocate a device field covering [-halo_lo, domain + halo_hi) per dim (a0 of SURVEY §8(a)).
  *   domain[3]    interior extent (Ni, Nj, Nk), each >= 1 (k: >= 1; use Nk = 1, halo 0 and
  *                k_invariant = 1 for 2D metric fields)
- *   halo_lo/hi   halo widths per dim, 0 <= h <= 16 in i (the left pad), any >= 0 in j, k
+ *   halo_lo/hi   halo widths per dim, 0 <= h <= 16 in i (f32: 32; the left pad), any >= 0 in j, k
  *   order        NULL = default {0, 2, 1}: i fastest, then k, then j (a j-slab halo is one
  *                contiguous block); or a permutation of {0,1,2}
  *                listing dims fastest -> slowest (order[0] must be 0)
  *   k_invariant  1: 2D field broadcast along k (requires domain[2] == 1, halo k == 0)
- * Layout: i rows start 16 elements left of i = 0 so that i = 0 is 128-byte aligned; the row
- * pitch is a multiple of 16 elements (128 B).  Memory is cudaMalloc'ed on `device` and zeroed.
+ *   dtype        OEC_F64 or OEC_F32
+ * Layout: i rows start 128 bytes (16 f64 / 32 f32 elements) left of i = 0 so that i = 0 is
+ * 128-byte aligned; the row pitch is a multiple of 128 bytes; halo_lo[0] may not exceed that pad.
+ * Memory is cudaMalloc'ed on `device` and zeroed.
  * out->owned = 1.  Errors: OEC_ERR_ARG (NULL/invalid), OEC_ERR_CUDA (allocation). */
 oec_status oec_field_create(const int64_t domain[3], const int32_t halo_lo[3], const int32_t halo_hi[3],
                             int32_t dtype, int32_t device, const int32_t order[3], int32_t k_invariant,

@@ -25,7 +25,8 @@ struct oec_decomp {
 namespace oec {
 namespace {
 
-__global__ void pack_kernel(FV src, Box b, double *buf) {
+template <class T>
+__global__ void pack_kernel(FVT<T> src, Box b, T *buf) {
     const long long ni = b.hi[0] - b.lo[0], nj = b.hi[1] - b.lo[1], nk = b.hi[2] - b.lo[2];
     const long long n = ni * nj * nk;
     for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n; t += (long long)gridDim.x * blockDim.x) {
@@ -33,7 +34,8 @@ __global__ void pack_kernel(FV src, Box b, double *buf) {
         buf[t] = src.p[i + j * src.sj + k * src.sk];
     }
 }
-__global__ void unpack_kernel(const double *buf, Box b, FO dst) {
+template <class T>
+__global__ void unpack_kernel(const T *buf, Box b, FOT<T> dst) {
     const long long ni = b.hi[0] - b.lo[0], nj = b.hi[1] - b.lo[1], nk = b.hi[2] - b.lo[2];
     const long long n = ni * nj * nk;
     for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n; t += (long long)gridDim.x * blockDim.x) {
@@ -41,7 +43,8 @@ __global__ void unpack_kernel(const double *buf, Box b, FO dst) {
         dst.p[i + j * dst.sj + k * dst.sk] = buf[t];
     }
 }
-__global__ void box_copy_kernel(FV src, FO dst, Box b) {
+template <class T>
+__global__ void box_copy_kernel(FVT<T> src, FOT<T> dst, Box b) {
     const long long ni = b.hi[0] - b.lo[0], nj = b.hi[1] - b.lo[1], nk = b.hi[2] - b.lo[2];
     const long long n = ni * nj * nk;
     for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n; t += (long long)gridDim.x * blockDim.x) {
@@ -60,24 +63,33 @@ unsigned grid_for(long long n) {
 
 }  // namespace
 
-cudaError_t launch_pack(const FV &src, const Box &b, double *buf, cudaStream_t s, int *launches) {
+template <class T>
+cudaError_t launch_pack(const FVT<T> &src, const Box &b, T *buf, cudaStream_t s, int *launches) {
     if (box_volume(b) <= 0) return cudaSuccess;
     pack_kernel<<<grid_for(box_volume(b)), 256, 0, s>>>(src, b, buf);
     ++*launches;
     return cudaGetLastError();
 }
-cudaError_t launch_unpack(const double *buf, const Box &b, const FO &dst, cudaStream_t s, int *launches) {
+template <class T>
+cudaError_t launch_unpack(const T *buf, const Box &b, const FOT<T> &dst, cudaStream_t s, int *launches) {
     if (box_volume(b) <= 0) return cudaSuccess;
     unpack_kernel<<<grid_for(box_volume(b)), 256, 0, s>>>(buf, b, dst);
     ++*launches;
     return cudaGetLastError();
 }
-cudaError_t launch_box_copy(const FV &src, const FO &dst, const Box &b, cudaStream_t s, int *launches) {
+template <class T>
+cudaError_t launch_box_copy(const FVT<T> &src, const FOT<T> &dst, const Box &b, cudaStream_t s, int *launches) {
     if (box_volume(b) <= 0) return cudaSuccess;
     box_copy_kernel<<<grid_for(box_volume(b)), 256, 0, s>>>(src, dst, b);
     ++*launches;
     return cudaGetLastError();
 }
+template cudaError_t launch_pack<double>(const FV &, const Box &, double *, cudaStream_t, int *);
+template cudaError_t launch_pack<float>(const FVf &, const Box &, float *, cudaStream_t, int *);
+template cudaError_t launch_unpack<double>(const double *, const Box &, const FO &, cudaStream_t, int *);
+template cudaError_t launch_unpack<float>(const float *, const Box &, const FOf &, cudaStream_t, int *);
+template cudaError_t launch_box_copy<double>(const FV &, const FO &, const Box &, cudaStream_t, int *);
+template cudaError_t launch_box_copy<float>(const FVf &, const FOf &, const Box &, cudaStream_t, int *);
 
 namespace {
 
@@ -150,7 +162,7 @@ struct Nccl {
 };
 Nccl g_nccl;
 std::mutex g_nccl_mu;
-constexpr int NCCL_FLOAT64 = 8;
+constexpr int NCCL_FLOAT32 = 7, NCCL_FLOAT64 = 8;
 
 bool load_nccl() {
     std::lock_guard<std::mutex> lock(g_nccl_mu);
@@ -171,22 +183,24 @@ bool load_nccl() {
 // staging for packed messages
 struct Stage {
     std::mutex mu;
-    double *p = nullptr;
-    size_t n = 0;
+    void *p = nullptr;
+    size_t n = 0;  // bytes
 };
 Stage g_hstage;
 
 bool is_kinv(const oec_field *f) { return f->stride[2] == 0 && f->ub[2] - f->lb[2] == 1 && f->lb[2] == 0; }
 
-oec_status view_of(const oec_field *f, FV *v) {
+template <class T>
+oec_status view_of(const oec_field *f, FVT<T> *v) {
     if (!f || !f->data) return set_error(OEC_ERR_ARG, "halo: NULL field");
-    if (f->dtype != OEC_F64) return set_error(OEC_ERR_DTYPE, "halo: dtype");
+    if (f->dtype != (sizeof(T) == 8 ? OEC_F64 : OEC_F32))
+        return set_error(OEC_ERR_DTYPE, "halo: all fields of one call must share one dtype");
     if (f->stride[0] != 1) return set_error(OEC_ERR_LAYOUT, "halo: stride[0] != 1");
     const int64_t sj = f->stride[1], sk = is_kinv(f) ? 0 : f->stride[2];
     const int64_t lbk = is_kinv(f) ? 0 : f->lb[2];
     const int64_t far = (f->ub[0] - f->lb[0]) + (f->ub[1] - f->lb[1]) * sj + (f->ub[2] - f->lb[2]) * sk;
     if (far > INT32_MAX || sj > INT32_MAX || sk > INT32_MAX) return set_error(OEC_ERR_LAYOUT, "halo: offsets exceed int32");
-    v->p = (const double *)((const char *)f->data - (f->lb[0] + f->lb[1] * sj + lbk * sk) * 8);
+    v->p = (const T *)((const char *)f->data - (f->lb[0] + f->lb[1] * sj + lbk * sk) * (int64_t)sizeof(T));
     v->sj = (int32_t)sj;
     v->sk = (int32_t)sk;
     return OEC_OK;
@@ -216,6 +230,116 @@ oec_status check_widths(const int32_t *wlo, const int32_t *whi) {
 }
 
 }  // namespace
+
+template <class T>
+oec_status halo_exchange_impl(oec_decomp *d, oec_field *const *fields, int32_t n, const int32_t width_lo[3],
+                              const int32_t width_hi[3], void *stream) {
+    oec_status st = check_widths(width_lo, width_hi);
+    if (st) return st;
+    auto plan = make_plan(d->gdom, d->px, d->py, d->rank, width_lo, width_hi);
+    set_launch_count(0);
+    if (plan.empty() || n == 0) return OEC_OK;
+    if (!d->comm) return set_error(OEC_ERR_NCCL, "oec_halo_exchange: decomposition has no NCCL communicator");
+    if (!load_nccl()) return set_error(OEC_ERR_NCCL, "oec_halo_exchange: libnccl.so.2 not loadable in this process");
+    cudaStream_t s = (cudaStream_t)stream;
+    // staging: one slot per (message, field)
+    std::vector<Box> boxes(plan.size() * n);
+    std::vector<FVT<T>> views(n);
+    size_t total = 0;
+    for (int f = 0; f < n; ++f) {
+        if (fields[f]->device < 0) return set_error(OEC_ERR_ARG, "oec_halo_exchange: fields must be device memory");
+        if ((st = view_of(fields[f], &views[f]))) return st;
+        for (size_t q = 0; q < plan.size(); ++q) {
+            if ((st = field_box(fields[f], plan[q], d->lo, &boxes[q * n + f]))) return st;
+            total += (size_t)box_volume(boxes[q * n + f]);
+        }
+    }
+    std::lock_guard<std::mutex> lock(g_hstage.mu);
+    if (g_hstage.n < total * sizeof(T)) {
+        if (g_hstage.p) cudaFree(g_hstage.p);
+        g_hstage.p = nullptr;
+        g_hstage.n = 0;
+        cudaError_t e = cudaMalloc(&g_hstage.p, total * sizeof(T));
+        if (e != cudaSuccess) return set_error(OEC_ERR_CUDA, "halo staging: %s", cudaGetErrorString(e));
+        g_hstage.n = total * sizeof(T);
+    }
+    std::vector<T *> bufs(plan.size() * n);
+    size_t off = 0;
+    for (size_t t = 0; t < bufs.size(); ++t) {
+        bufs[t] = (T *)g_hstage.p + off;
+        off += (size_t)box_volume(boxes[t]);
+    }
+    constexpr int NCCL_DT = sizeof(T) == 8 ? NCCL_FLOAT64 : NCCL_FLOAT32;
+    int launches = 0;
+    for (int phase = 0; phase < 2; ++phase) {
+        for (size_t q = 0; q < plan.size(); ++q)
+            if (plan[q].phase == phase && plan[q].is_send)
+                for (int f = 0; f < n; ++f) {
+                    cudaError_t e = launch_pack(views[f], boxes[q * n + f], bufs[q * n + f], s, &launches);
+                    if (e != cudaSuccess) return set_error(OEC_ERR_CUDA, "halo pack: %s", cudaGetErrorString(e));
+                }
+        int r = g_nccl.gstart();
+        for (size_t q = 0; q < plan.size() && r == 0; ++q) {
+            if (plan[q].phase != phase) continue;
+            for (int f = 0; f < n && r == 0; ++f) {
+                const size_t cnt = (size_t)box_volume(boxes[q * n + f]);
+                r = plan[q].is_send ? g_nccl.send(bufs[q * n + f], cnt, NCCL_DT, plan[q].peer, d->comm, s)
+                                    : g_nccl.recv(bufs[q * n + f], cnt, NCCL_DT, plan[q].peer, d->comm, s);
+            }
+        }
+        int r2 = g_nccl.gend();
+        if (r || r2)
+            return set_error(OEC_ERR_NCCL, "oec_halo_exchange: NCCL error %d (%s)", r ? r : r2,
+                             g_nccl.errstr ? g_nccl.errstr(r ? r : r2) : "?");
+        for (size_t q = 0; q < plan.size(); ++q)
+            if (plan[q].phase == phase && !plan[q].is_send)
+                for (int f = 0; f < n; ++f) {
+                    FOT<T> o{(T *)views[f].p, views[f].sj, views[f].sk};
+                    cudaError_t e = launch_unpack(bufs[q * n + f], boxes[q * n + f], o, s, &launches);
+                    if (e != cudaSuccess) return set_error(OEC_ERR_CUDA, "halo unpack: %s", cudaGetErrorString(e));
+                }
+    }
+    set_launch_count(launches);
+    return OEC_OK;
+}
+
+template <class T>
+oec_status halo_exchange_local_impl(const int64_t global_domain[3], int32_t px, int32_t py, oec_field *const *fields,
+                                    int32_t n, const int32_t width_lo[3], const int32_t width_hi[3], void *stream) {
+    oec_status st = check_widths(width_lo, width_hi);
+    if (st) return st;
+    cudaStream_t s = (cudaStream_t)stream;
+    const int R = px * py;
+    int launches = 0;
+    for (int phase = 0; phase < 2; ++phase) {
+        for (int r = 0; r < R; ++r) {
+            auto plan = make_plan(global_domain, px, py, r, width_lo, width_hi);
+            for (auto &m : plan) {
+                if (m.phase != phase || m.is_send) continue;
+                for (int f = 0; f < n; ++f) {
+                    const oec_field *src = fields[m.peer * n + f];
+                    oec_field *dst = fields[r * n + f];
+                    int64_t org_d[3], org_s[3], tmp[3];
+                    subdomain(global_domain, px, py, r, org_d, tmp);
+                    subdomain(global_domain, px, py, m.peer, org_s, tmp);
+                    FVT<T> vs, vd;
+                    Box bd, bs;
+                    if ((st = view_of(src, &vs)) || (st = view_of(dst, &vd)) || (st = field_box(dst, m, org_d, &bd)) ||
+                        (st = field_box(src, m, org_s, &bs)))
+                        return st;
+                    // shift the source origin so that the destination's local box indexes it
+                    vs.p += (int64_t)(bs.lo[0] - bd.lo[0]) + (int64_t)(bs.lo[1] - bd.lo[1]) * vs.sj;
+                    FOT<T> o{(T *)vd.p, vd.sj, vd.sk};
+                    cudaError_t e = launch_box_copy(vs, o, bd, s, &launches);
+                    if (e != cudaSuccess) return set_error(OEC_ERR_CUDA, "halo copy: %s", cudaGetErrorString(e));
+                }
+            }
+        }
+    }
+    set_launch_count(launches);
+    return OEC_OK;
+}
+
 }  // namespace oec
 
 using namespace oec;
@@ -263,110 +387,18 @@ oec_status oec_decomp_plan(const oec_decomp *d, const int32_t width_lo[3], const
 oec_status oec_halo_exchange(oec_decomp *d, oec_field *const *fields, int32_t n, const int32_t width_lo[3],
                              const int32_t width_hi[3], void *stream) {
     if (!d || (!fields && n > 0) || n < 0) return set_error(OEC_ERR_ARG, "oec_halo_exchange: bad arguments");
-    oec_status st = check_widths(width_lo, width_hi);
-    if (st) return st;
-    auto plan = make_plan(d->gdom, d->px, d->py, d->rank, width_lo, width_hi);
-    set_launch_count(0);
-    if (plan.empty() || n == 0) return OEC_OK;
-    if (!d->comm) return set_error(OEC_ERR_NCCL, "oec_halo_exchange: decomposition has no NCCL communicator");
-    if (!load_nccl()) return set_error(OEC_ERR_NCCL, "oec_halo_exchange: libnccl.so.2 not loadable in this process");
-    cudaStream_t s = (cudaStream_t)stream;
-    // staging: one slot per (message, field)
-    std::vector<Box> boxes(plan.size() * n);
-    std::vector<FV> views(n);
-    size_t total = 0;
-    for (int f = 0; f < n; ++f) {
-        if (fields[f]->device < 0) return set_error(OEC_ERR_ARG, "oec_halo_exchange: fields must be device memory");
-        if ((st = view_of(fields[f], &views[f]))) return st;
-        for (size_t q = 0; q < plan.size(); ++q) {
-            if ((st = field_box(fields[f], plan[q], d->lo, &boxes[q * n + f]))) return st;
-            total += (size_t)box_volume(boxes[q * n + f]);
-        }
-    }
-    std::lock_guard<std::mutex> lock(g_hstage.mu);
-    if (g_hstage.n < total) {
-        if (g_hstage.p) cudaFree(g_hstage.p);
-        g_hstage.p = nullptr;
-        g_hstage.n = 0;
-        cudaError_t e = cudaMalloc(&g_hstage.p, total * sizeof(double));
-        if (e != cudaSuccess) return set_error(OEC_ERR_CUDA, "halo staging: %s", cudaGetErrorString(e));
-        g_hstage.n = total;
-    }
-    std::vector<double *> bufs(plan.size() * n);
-    size_t off = 0;
-    for (size_t t = 0; t < bufs.size(); ++t) {
-        bufs[t] = g_hstage.p + off;
-        off += (size_t)box_volume(boxes[t]);
-    }
-    int launches = 0;
-    for (int phase = 0; phase < 2; ++phase) {
-        for (size_t q = 0; q < plan.size(); ++q)
-            if (plan[q].phase == phase && plan[q].is_send)
-                for (int f = 0; f < n; ++f) {
-                    cudaError_t e = launch_pack(views[f], boxes[q * n + f], bufs[q * n + f], s, &launches);
-                    if (e != cudaSuccess) return set_error(OEC_ERR_CUDA, "halo pack: %s", cudaGetErrorString(e));
-                }
-        int r = g_nccl.gstart();
-        for (size_t q = 0; q < plan.size() && r == 0; ++q) {
-            if (plan[q].phase != phase) continue;
-            for (int f = 0; f < n && r == 0; ++f) {
-                const size_t cnt = (size_t)box_volume(boxes[q * n + f]);
-                r = plan[q].is_send ? g_nccl.send(bufs[q * n + f], cnt, NCCL_FLOAT64, plan[q].peer, d->comm, s)
-                                    : g_nccl.recv(bufs[q * n + f], cnt, NCCL_FLOAT64, plan[q].peer, d->comm, s);
-            }
-        }
-        int r2 = g_nccl.gend();
-        if (r || r2)
-            return set_error(OEC_ERR_NCCL, "oec_halo_exchange: NCCL error %d (%s)", r ? r : r2,
-                             g_nccl.errstr ? g_nccl.errstr(r ? r : r2) : "?");
-        for (size_t q = 0; q < plan.size(); ++q)
-            if (plan[q].phase == phase && !plan[q].is_send)
-                for (int f = 0; f < n; ++f) {
-                    FO o{(double *)views[f].p, views[f].sj, views[f].sk};
-                    cudaError_t e = launch_unpack(bufs[q * n + f], boxes[q * n + f], o, s, &launches);
-                    if (e != cudaSuccess) return set_error(OEC_ERR_CUDA, "halo unpack: %s", cudaGetErrorString(e));
-                }
-    }
-    set_launch_count(launches);
-    return OEC_OK;
+    if (n > 0 && !fields[0]) return set_error(OEC_ERR_ARG, "oec_halo_exchange: NULL field");
+    if (n > 0 && fields[0]->dtype == OEC_F32) return halo_exchange_impl<float>(d, fields, n, width_lo, width_hi, stream);
+    return halo_exchange_impl<double>(d, fields, n, width_lo, width_hi, stream);
 }
 
 oec_status oec_halo_exchange_local(const int64_t global_domain[3], int32_t px, int32_t py, oec_field *const *fields,
                                    int32_t n, const int32_t width_lo[3], const int32_t width_hi[3], void *stream) {
-    if (!global_domain || !fields || n < 1 || px < 1 || py < 1)
+    if (!global_domain || !fields || n < 1 || px < 1 || py < 1 || !fields[0])
         return set_error(OEC_ERR_ARG, "oec_halo_exchange_local: bad arguments");
-    oec_status st = check_widths(width_lo, width_hi);
-    if (st) return st;
-    cudaStream_t s = (cudaStream_t)stream;
-    const int R = px * py;
-    int launches = 0;
-    for (int phase = 0; phase < 2; ++phase) {
-        for (int r = 0; r < R; ++r) {
-            auto plan = make_plan(global_domain, px, py, r, width_lo, width_hi);
-            for (auto &m : plan) {
-                if (m.phase != phase || m.is_send) continue;
-                for (int f = 0; f < n; ++f) {
-                    const oec_field *src = fields[m.peer * n + f];
-                    oec_field *dst = fields[r * n + f];
-                    int64_t org_d[3], org_s[3], tmp[3];
-                    subdomain(global_domain, px, py, r, org_d, tmp);
-                    subdomain(global_domain, px, py, m.peer, org_s, tmp);
-                    FV vs, vd;
-                    Box bd, bs;
-                    if ((st = view_of(src, &vs)) || (st = view_of(dst, &vd)) || (st = field_box(dst, m, org_d, &bd)) ||
-                        (st = field_box(src, m, org_s, &bs)))
-                        return st;
-                    // shift the source origin so that the destination's local box indexes it
-                    vs.p += (int64_t)(bs.lo[0] - bd.lo[0]) + (int64_t)(bs.lo[1] - bd.lo[1]) * vs.sj;
-                    FO o{(double *)vd.p, vd.sj, vd.sk};
-                    cudaError_t e = launch_box_copy(vs, o, bd, s, &launches);
-                    if (e != cudaSuccess) return set_error(OEC_ERR_CUDA, "halo copy: %s", cudaGetErrorString(e));
-                }
-            }
-        }
-    }
-    set_launch_count(launches);
-    return OEC_OK;
+    if (fields[0]->dtype == OEC_F32)
+        return halo_exchange_local_impl<float>(global_domain, px, py, fields, n, width_lo, width_hi, stream);
+    return halo_exchange_local_impl<double>(global_domain, px, py, fields, n, width_lo, width_hi, stream);
 }
 
 }  // extern "C"

@@ -7,7 +7,7 @@
 //  * hdiff_tma    -- default B200 design: persistent CTAs of NW
 //                    independent warps; each warp owns an S-deep ring of shared-memory slots fed by
 //                    TMA (cp.async.bulk.tensor, mbarrier complete_tx).  A work item is a W x JB tile
-//                    of one k-plane: one TMA box of `in` ((W+4) x (JB+4), halo included, OOB
+//                    of one k-plane: one TMA box of `in` ((W+2LP) x (JB+4), halo included, OOB
 //                    zero-filled) and one of `coeff` (W x JB).  The warp walks the tile along j,
 //                    each lane reading its V columns plus the 2-wide halo straight from shared
 //                    memory (16-byte LDS, conflict-free) and rolling lap/flx/fly in registers.
@@ -55,6 +55,32 @@
 #ifndef HDL_NW
 #define HDL_NW 12
 #endif
+// f32: V doubled so a tile row is as many bytes as in f64 (the TMA box is <= 256 elements
+// wide: 32 V + 8 <= 256 -> V <= 7; V % 4 == 0 for 16-byte shared-memory loads)
+#ifndef HF_V
+#define HF_V 4
+#endif
+#ifndef HF_JB
+#define HF_JB 4
+#endif
+#ifndef HF_S
+#define HF_S 2
+#endif
+#ifndef HF_NW
+#define HF_NW 12
+#endif
+#ifndef HFL_V
+#define HFL_V 4
+#endif
+#ifndef HFL_JB
+#define HFL_JB 2
+#endif
+#ifndef HFL_S
+#define HFL_S 2
+#endif
+#ifndef HFL_NW
+#define HFL_NW 12
+#endif
 #ifndef HD_LARGE_POINTS
 #define HD_LARGE_POINTS (2ll << 20)
 #endif
@@ -83,21 +109,24 @@ extern "C" int oec_debug_hdiff_trace(unsigned long long *out) {
 namespace oec {
 namespace {
 
-__device__ __forceinline__ double ld(const FV &f, int i, int j, int k) { return __ldg(f.p + (i + j * f.sj + k * f.sk)); }
+template <class T>
+__device__ __forceinline__ T ld(const FVT<T> &f, int i, int j, int k) { return __ldg(f.p + (i + j * f.sj + k * f.sk)); }
 
-__device__ __forceinline__ double lap_pt(double c, double w, double e, double s, double n) {
+template <class T>
+__device__ __forceinline__ T lap_pt(T c, T w, T e, T s, T n) {
     // lap(i,j) = ((in(i-1,j) + in(i+1,j)) + (in(i,j-1) + in(i,j+1))) - 4 in(i,j)
-    return ((w + e) + (s + n)) - 4.0 * c;
+    return ((w + e) + (s + n)) - T(4.0) * c;
 }
-__device__ __forceinline__ double limit(double f, double din) { return (f * din > 0.0) ? 0.0 : f; }
+template <class T>
+__device__ __forceinline__ T limit(T f, T din) { return (f * din > T(0.0)) ? T(0.0) : f; }
 
 // ---------------------------------------------------------------------------------------------
 // paper execution model
 // ---------------------------------------------------------------------------------------------
 // UJ > 1: stencil unrolling along j: one thread updates UJ consecutive rows; the
 // Laplacians and loads the rows share are computed once (common-subexpression elimination).
-template <int UJ>
-__global__ void __launch_bounds__(128) hdiff_naive(FV in, FV coeff, FO out, Dom d) {
+template <class T, int UJ>
+__global__ void __launch_bounds__(128) hdiff_naive(FVT<T> in, FVT<T> coeff, FOT<T> out, Dom d) {
     const int i = d.lo[0] + blockIdx.x * 32 + threadIdx.x;
     const int j0 = d.lo[1] + (blockIdx.y * 4 + threadIdx.y) * UJ;
     const int k = d.lo[2] + blockIdx.z;
@@ -105,16 +134,16 @@ __global__ void __launch_bounds__(128) hdiff_naive(FV in, FV coeff, FO out, Dom 
     auto L = [&](int a, int b) {
         return lap_pt(ld(in, a, b, k), ld(in, a - 1, b, k), ld(in, a + 1, b, k), ld(in, a, b - 1, k), ld(in, a, b + 1, k));
     };
-    double r[UJ];
+    T r[UJ];
 #pragma unroll
     for (int u = 0; u < UJ; ++u) {
         const int j = min(j0 + u, d.hi[1] - 1);
-        const double c0 = ld(in, i, j, k);
-        const double l0 = L(i, j), le = L(i + 1, j), lw = L(i - 1, j), ln = L(i, j + 1), ls = L(i, j - 1);
-        const double flx = limit(le - l0, ld(in, i + 1, j, k) - c0);
-        const double flxm = limit(l0 - lw, c0 - ld(in, i - 1, j, k));
-        const double fly = limit(ln - l0, ld(in, i, j + 1, k) - c0);
-        const double flym = limit(l0 - ls, c0 - ld(in, i, j - 1, k));
+        const T c0 = ld(in, i, j, k);
+        const T l0 = L(i, j), le = L(i + 1, j), lw = L(i - 1, j), ln = L(i, j + 1), ls = L(i, j - 1);
+        const T flx = limit(le - l0, ld(in, i + 1, j, k) - c0);
+        const T flxm = limit(l0 - lw, c0 - ld(in, i - 1, j, k));
+        const T fly = limit(ln - l0, ld(in, i, j + 1, k) - c0);
+        const T flym = limit(l0 - ls, c0 - ld(in, i, j - 1, k));
         r[u] = c0 - ld(coeff, i, j, k) * ((flx - flxm) + (fly - flym));
     }
 #pragma unroll
@@ -125,15 +154,19 @@ __global__ void __launch_bounds__(128) hdiff_naive(FV in, FV coeff, FO out, Dom 
 // ---------------------------------------------------------------------------------------------
 // rolling kernel
 // ---------------------------------------------------------------------------------------------
-template <int V>
-struct Vec;
-template <>
-struct Vec<1> {
-    static __device__ __forceinline__ void load(const double *p, double *v) { v[0] = __ldg(p); }
-    static __device__ __forceinline__ void store(double *p, const double *v) { p[0] = v[0]; }
+template <class T, int V>
+struct Vec {  // generic: scalar accesses
+    static __device__ __forceinline__ void load(const T *p, T *v) {
+#pragma unroll
+        for (int x = 0; x < V; ++x) v[x] = __ldg(p + x);
+    }
+    static __device__ __forceinline__ void store(T *p, const T *v) {
+#pragma unroll
+        for (int x = 0; x < V; ++x) p[x] = v[x];
+    }
 };
 template <>
-struct Vec<2> {
+struct Vec<double, 2> {
     static __device__ __forceinline__ void load(const double *p, double *v) {
         double2 t = __ldg(reinterpret_cast<const double2 *>(p));
         v[0] = t.x;
@@ -143,36 +176,59 @@ struct Vec<2> {
         *reinterpret_cast<double2 *>(p) = make_double2(v[0], v[1]);
     }
 };
-
 template <>
-struct Vec<4> {
+struct Vec<double, 4> {
     static __device__ __forceinline__ void load(const double *p, double *v) {
-        Vec<2>::load(p, v);
-        Vec<2>::load(p + 2, v + 2);
+        Vec<double, 2>::load(p, v);
+        Vec<double, 2>::load(p + 2, v + 2);
     }
     static __device__ __forceinline__ void store(double *p, const double *v) {
-        Vec<2>::store(p, v);
-        Vec<2>::store(p + 2, v + 2);
+        Vec<double, 2>::store(p, v);
+        Vec<double, 2>::store(p + 2, v + 2);
+    }
+};
+template <>
+struct Vec<float, 4> {
+    static __device__ __forceinline__ void load(const float *p, float *v) {
+        float4 t = __ldg(reinterpret_cast<const float4 *>(p));
+        v[0] = t.x;
+        v[1] = t.y;
+        v[2] = t.z;
+        v[3] = t.w;
+    }
+    static __device__ __forceinline__ void store(float *p, const float *v) {
+        *reinterpret_cast<float4 *>(p) = make_float4(v[0], v[1], v[2], v[3]);
+    }
+};
+template <>
+struct Vec<float, 8> {
+    static __device__ __forceinline__ void load(const float *p, float *v) {
+        Vec<float, 4>::load(p, v);
+        Vec<float, 4>::load(p + 4, v + 4);
+    }
+    static __device__ __forceinline__ void store(float *p, const float *v) {
+        Vec<float, 4>::store(p, v);
+        Vec<float, 4>::store(p + 4, v + 4);
     }
 };
 
 // raw row as loaded: V own values + (lane 0) 2 left-halo values + (lane 31) 2 right-halo values
-template <int V>
+template <class T, int V>
 struct RawRow {
-    double v[V];
-    double h[2];
+    T v[V];
+    T h[2];
 };
 
-template <int V>
-__device__ __forceinline__ void load_row(const double *rowp, int i_own, int lane, int i_end_in, int ib, RawRow<V> &r) {
+template <class T, int V>
+__device__ __forceinline__ void load_row(const T *rowp, int i_own, int lane, int i_end_in, int ib, RawRow<T, V> &r) {
     // rowp: pointer to element (0, j, k); i_own = ib + lane*V; valid `in` columns: i < i_end_in
     if (i_own + V <= i_end_in) {
-        Vec<V>::load(rowp + i_own, r.v);
+        Vec<T, V>::load(rowp + i_own, r.v);
     } else {
 #pragma unroll
-        for (int v = 0; v < V; ++v) r.v[v] = (i_own + v < i_end_in) ? __ldg(rowp + i_own + v) : 0.0;
+        for (int v = 0; v < V; ++v) r.v[v] = (i_own + v < i_end_in) ? __ldg(rowp + i_own + v) : T(0.0);
     }
-    r.h[0] = r.h[1] = 0.0;
+    r.h[0] = r.h[1] = T(0.0);
     if (lane == 0) {
         r.h[0] = __ldg(rowp + ib - 2);
         r.h[1] = __ldg(rowp + ib - 1);
@@ -184,12 +240,12 @@ __device__ __forceinline__ void load_row(const double *rowp, int i_own, int lane
 }
 
 // extended row: e[x + 2] = in(i_own + x), x in [-2, V+1]
-template <int V>
-__device__ __forceinline__ void extend(const RawRow<V> &r, int lane, double *e) {
+template <class T, int V>
+__device__ __forceinline__ void extend(const RawRow<T, V> &r, int lane, T *e) {
     constexpr unsigned FULL = 0xffffffffu;
 #pragma unroll
     for (int v = 0; v < V; ++v) e[v + 2] = r.v[v];
-    double l1, l2, r1, r2;
+    T l1, l2, r1, r2;
     if (V >= 2) {
         l2 = __shfl_up_sync(FULL, r.v[V - 2 < 0 ? 0 : V - 2], 1);
         l1 = __shfl_up_sync(FULL, r.v[V - 1], 1);
@@ -202,8 +258,8 @@ __device__ __forceinline__ void extend(const RawRow<V> &r, int lane, double *e) 
         r2 = __shfl_down_sync(FULL, r.v[0], 2);
     }
     if (V == 1) {  // lanes 1 and 30 take the halo values held by lanes 0 and 31
-        const double hl = __shfl_sync(FULL, r.h[1], 0);
-        const double hr = __shfl_sync(FULL, r.h[0], 31);
+        const T hl = __shfl_sync(FULL, r.h[1], 0);
+        const T hr = __shfl_sync(FULL, r.h[0], 31);
         if (lane == 1) l2 = hl;
         if (lane == 30) r2 = hr;
     }
@@ -221,8 +277,8 @@ __device__ __forceinline__ void extend(const RawRow<V> &r, int lane, double *e) 
     e[V + 3] = r2;
 }
 
-template <int V, int JB, int P>
-__global__ void __launch_bounds__(128) hdiff_roll(FV in, FV coeff, FO out, Dom d, int nseg, int nchunk) {
+template <class T, int V, int JB, int P>
+__global__ void __launch_bounds__(128) hdiff_roll(FVT<T> in, FVT<T> coeff, FOT<T> out, Dom d, int nseg, int nchunk) {
     constexpr int W = 32 * V;
     const int lane = threadIdx.x & 31;
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -235,27 +291,27 @@ __global__ void __launch_bounds__(128) hdiff_roll(FV in, FV coeff, FO out, Dom d
     const int i_end_in = d.hi[0] + 2;  // `in` columns needed: [ib-2, min(ib+W, hi0)+2)
     const int j0 = d.lo[1] + chunk * JB;
     const int j1 = min(j0 + JB, d.hi[1]);
-    const double *in_k = in.p + k * in.sk;
-    const double *cf_k = coeff.p + k * coeff.sk;
-    double *out_k = out.p + k * out.sk;
+    const T *in_k = in.p + k * in.sk;
+    const T *cf_k = coeff.p + k * coeff.sk;
+    T *out_k = out.p + k * out.sk;
 
-    double E0[V + 4], E1[V + 4], E2[V + 4];  // in rows j, j+1, j+2 (extended)
-    double Lj[V + 2];                        // lap row j at i_own-1 .. i_own+V
-    double FYm[V];                           // fly(j-1) at own points
+    T E0[V + 4], E1[V + 4], E2[V + 4];  // in rows j, j+1, j+2 (extended)
+    T Lj[V + 2];                        // lap row j at i_own-1 .. i_own+V
+    T FYm[V];                           // fly(j-1) at own points
 
     // ---- warm-up: rows j0-2 .. j0+1 ----
     {
-        RawRow<V> r;
-        double Em2[V + 4], Em1[V + 4];
-        load_row<V>(in_k + (j0 - 2) * in.sj, i_own, lane, i_end_in, ib, r);
-        extend<V>(r, lane, Em2);
-        load_row<V>(in_k + (j0 - 1) * in.sj, i_own, lane, i_end_in, ib, r);
-        extend<V>(r, lane, Em1);
-        load_row<V>(in_k + j0 * in.sj, i_own, lane, i_end_in, ib, r);
-        extend<V>(r, lane, E0);
-        load_row<V>(in_k + (j0 + 1) * in.sj, i_own, lane, i_end_in, ib, r);
-        extend<V>(r, lane, E1);
-        double Lm[V];  // lap(j0-1) at own points
+        RawRow<T, V> r;
+        T Em2[V + 4], Em1[V + 4];
+        load_row<T, V>(in_k + (j0 - 2) * in.sj, i_own, lane, i_end_in, ib, r);
+        extend<T, V>(r, lane, Em2);
+        load_row<T, V>(in_k + (j0 - 1) * in.sj, i_own, lane, i_end_in, ib, r);
+        extend<T, V>(r, lane, Em1);
+        load_row<T, V>(in_k + j0 * in.sj, i_own, lane, i_end_in, ib, r);
+        extend<T, V>(r, lane, E0);
+        load_row<T, V>(in_k + (j0 + 1) * in.sj, i_own, lane, i_end_in, ib, r);
+        extend<T, V>(r, lane, E1);
+        T Lm[V];  // lap(j0-1) at own points
 #pragma unroll
         for (int x = 0; x < V; ++x) Lm[x] = lap_pt(Em1[x + 2], Em1[x + 1], Em1[x + 3], Em2[x + 2], E0[x + 2]);
 #pragma unroll
@@ -266,19 +322,19 @@ __global__ void __launch_bounds__(128) hdiff_roll(FV in, FV coeff, FO out, Dom d
     }
 
     // ---- prefetch ring: slot s holds in row (j+2) and coeff row j for step j = j0 + s (mod P) ----
-    RawRow<V> ring_in[P];
-    double ring_cf[P][V];
+    RawRow<T, V> ring_in[P];
+    T ring_cf[P][V];
     const bool own_valid = i_own < d.hi[0];
 #pragma unroll
     for (int s = 0; s < P; ++s) {
         const int j = j0 + s;
         if (j < j1) {
-            load_row<V>(in_k + (j + 2) * in.sj, i_own, lane, i_end_in, ib, ring_in[s]);
+            load_row<T, V>(in_k + (j + 2) * in.sj, i_own, lane, i_end_in, ib, ring_in[s]);
             if (own_valid) {
-                if (i_own + V <= d.hi[0]) Vec<V>::load(cf_k + j * coeff.sj + i_own, ring_cf[s]);
+                if (i_own + V <= d.hi[0]) Vec<T, V>::load(cf_k + j * coeff.sj + i_own, ring_cf[s]);
                 else {
 #pragma unroll
-                    for (int v = 0; v < V; ++v) ring_cf[s][v] = (i_own + v < d.hi[0]) ? __ldg(cf_k + j * coeff.sj + i_own + v) : 0.0;
+                    for (int v = 0; v < V; ++v) ring_cf[s][v] = (i_own + v < d.hi[0]) ? __ldg(cf_k + j * coeff.sj + i_own + v) : T(0.0);
                 }
             }
         }
@@ -289,41 +345,41 @@ __global__ void __launch_bounds__(128) hdiff_roll(FV in, FV coeff, FO out, Dom d
         for (int s = 0; s < P; ++s) {
             const int j = jb + s;
             if (j < j1) {  // warp-uniform
-                extend<V>(ring_in[s], lane, E2);
-                double cf[V];
+                extend<T, V>(ring_in[s], lane, E2);
+                T cf[V];
 #pragma unroll
                 for (int v = 0; v < V; ++v) cf[v] = ring_cf[s][v];
                 // refill this slot with step j + P
                 const int jn = j + P;
                 if (jn < j1) {
-                    load_row<V>(in_k + (jn + 2) * in.sj, i_own, lane, i_end_in, ib, ring_in[s]);
+                    load_row<T, V>(in_k + (jn + 2) * in.sj, i_own, lane, i_end_in, ib, ring_in[s]);
                     if (own_valid) {
-                        if (i_own + V <= d.hi[0]) Vec<V>::load(cf_k + jn * coeff.sj + i_own, ring_cf[s]);
+                        if (i_own + V <= d.hi[0]) Vec<T, V>::load(cf_k + jn * coeff.sj + i_own, ring_cf[s]);
                         else {
 #pragma unroll
                             for (int v = 0; v < V; ++v)
-                                ring_cf[s][v] = (i_own + v < d.hi[0]) ? __ldg(cf_k + jn * coeff.sj + i_own + v) : 0.0;
+                                ring_cf[s][v] = (i_own + v < d.hi[0]) ? __ldg(cf_k + jn * coeff.sj + i_own + v) : T(0.0);
                         }
                     }
                 }
                 // lap(j+1) at i_own-1 .. i_own+V
-                double L1[V + 2];
+                T L1[V + 2];
 #pragma unroll
                 for (int y = 0; y < V + 2; ++y) L1[y] = lap_pt(E1[y + 1], E1[y], E1[y + 2], E0[y + 1], E2[y + 1]);
                 // flx(j) at i_own-1 .. i_own+V-1:  FX[y] <-> i_own + y - 1
-                double FX[V + 1];
+                T FX[V + 1];
 #pragma unroll
                 for (int y = 0; y < V + 1; ++y) FX[y] = limit(Lj[y + 1] - Lj[y], E0[y + 2] - E0[y + 1]);
                 // fly(j) at own points
-                double FY[V];
+                T FY[V];
 #pragma unroll
                 for (int x = 0; x < V; ++x) FY[x] = limit(L1[x + 1] - Lj[x + 1], E1[x + 2] - E0[x + 2]);
-                double o[V];
+                T o[V];
 #pragma unroll
                 for (int x = 0; x < V; ++x) o[x] = E0[x + 2] - cf[x] * ((FX[x + 1] - FX[x]) + (FY[x] - FYm[x]));
                 if (own_valid) {
-                    double *op = out_k + j * out.sj + i_own;
-                    if (i_own + V <= d.hi[0]) Vec<V>::store(op, o);
+                    T *op = out_k + j * out.sj + i_own;
+                    if (i_own + V <= d.hi[0]) Vec<T, V>::store(op, o);
                     else {
 #pragma unroll
                         for (int v = 0; v < V; ++v)
@@ -348,52 +404,71 @@ __global__ void __launch_bounds__(128) hdiff_roll(FV in, FV coeff, FO out, Dom d
 // ---------------------------------------------------------------------------------------------
 // TMA-fed kernel
 // ---------------------------------------------------------------------------------------------
-template <int V, int JB, int S, int NW>
+// The `in` box starts LP columns left of the tile: TMA needs the inner start coordinate on a 16-byte
+// boundary (measured: tools/micro/tma_f32.cu -- an f32 box starting 8 bytes off a 16-byte boundary
+// faults with an illegal instruction), so LP = 16 bytes of elements (2 f64, 4 f32) >= the 2-wide
+// halo, and a row is RW = W + 2 LP elements (a 16-byte multiple).
+template <class T, int V, int JB, int S, int NW>
 struct TmaCfg {
     static constexpr int W = 32 * V;
-    static constexpr int IN_ELEMS = (JB + 4) * (W + 4);
-    static constexpr int IN_BYTES = IN_ELEMS * 8;
-    static constexpr int CF_BYTES = JB * W * 8;
+    static constexpr int LP = 16 / (int)sizeof(T);
+    static constexpr int RW = W + 2 * LP;
+    static constexpr int IN_ELEMS = (JB + 4) * RW;
+    static constexpr int IN_BYTES = IN_ELEMS * (int)sizeof(T);
+    static constexpr int CF_BYTES = JB * W * (int)sizeof(T);
     static constexpr int IN_PAD = (IN_BYTES + 127) / 128 * 128;
     static constexpr int CF_PAD = (CF_BYTES + 127) / 128 * 128;
     static constexpr int SLOT = IN_PAD + CF_PAD;
     static constexpr int SMEM = NW * S * SLOT + NW * S * 8;
 };
 
-template <int V>
-__device__ __forceinline__ void lds_row(const double *row, int lane, double *e) {
-    // e[x] = row[lane*V + x], x in [0, V+4)  (row element x <-> i = ib - 2 + x)
-    const double *p = row + lane * V;
-    if constexpr (V % 2 == 0) {
+template <class T, int V, int LP>
+__device__ __forceinline__ void lds_row(const T *row, int lane, T *e) {
+    // e[x] = row[lane*V + (LP-2) + x], x in [0, V+4)  (row element y <-> i = ib - LP + y); widest aligned LDS
+    const T *p = row + lane * V;
+    if constexpr (sizeof(T) == 4 && V % 4 == 0) {  // LP = 4: 16-byte loads of V+8 elements, shifted by 2
+        T t[V + 8];
+#pragma unroll
+        for (int x = 0; x < V + 8; x += 4) {
+            const float4 q = *reinterpret_cast<const float4 *>(p + x);
+            t[x] = q.x;
+            t[x + 1] = q.y;
+            t[x + 2] = q.z;
+            t[x + 3] = q.w;
+        }
+#pragma unroll
+        for (int x = 0; x < V + 4; ++x) e[x] = t[x + 2];
+    } else if constexpr (sizeof(T) == 8 && V % 2 == 0) {  // LP = 2: 16-byte loads, no shift
 #pragma unroll
         for (int x = 0; x < V + 4; x += 2) {
-            const double2 t = *reinterpret_cast<const double2 *>(p + x);
-            e[x] = t.x;
-            e[x + 1] = t.y;
+            const double2 q = *reinterpret_cast<const double2 *>(p + x);
+            e[x] = q.x;
+            e[x + 1] = q.y;
         }
     } else {
 #pragma unroll
-        for (int x = 0; x < V + 4; ++x) e[x] = p[x];
+        for (int x = 0; x < V + 4; ++x) e[x] = p[(LP - 2) + x];
     }
 }
 
-// One W x JB tile from shared memory: rows 0..JB+3 of `tin` are j0-2 .. j0+JB+1 (each W+4 wide,
-// element x <-> i = ib-2+x), `tcf` holds coeff rows j0 .. j0+JB-1 (W wide).  FULL: all JB rows are
+// One W x JB tile from shared memory: rows 0..JB+3 of `tin` are j0-2 .. j0+JB+1 (each RW wide,
+// element y <-> i = ib-LP+y), `tcf` holds coeff rows j0 .. j0+JB-1 (W wide).  FULL: all JB rows are
 // in the domain -> the row loop is fully unrolled without checks (registers renamed, no moves).
-template <int V, int JB, bool FULL>
-__device__ __forceinline__ void hdiff_tile(const double *tin, const double *tcf, double *out_k, int sj, int j0,
+template <class T, int V, int JB, int LP, bool FULL>
+__device__ __forceinline__ void hdiff_tile(const T *tin, const T *tcf, T *out_k, int sj, int j0,
                                            int nrows, int i_own, int hi0, int lane) {
     constexpr int W = 32 * V;
+    constexpr int RW = W + 2 * LP;
     const bool own_valid = i_own < hi0;
     const bool own_full = i_own + V <= hi0;
     const bool warp_full = __all_sync(0xffffffffu, own_full);
-    double E0[V + 4], E1[V + 4], E2[V + 4], Lj[V + 2], FYm[V];
+    T E0[V + 4], E1[V + 4], E2[V + 4], Lj[V + 2], FYm[V];
     {
-        double Em2[V + 4], Em1[V + 4], Lm[V];
-        lds_row<V>(tin + 0 * (W + 4), lane, Em2);
-        lds_row<V>(tin + 1 * (W + 4), lane, Em1);
-        lds_row<V>(tin + 2 * (W + 4), lane, E0);
-        lds_row<V>(tin + 3 * (W + 4), lane, E1);
+        T Em2[V + 4], Em1[V + 4], Lm[V];
+        lds_row<T, V, LP>(tin + 0 * RW, lane, Em2);
+        lds_row<T, V, LP>(tin + 1 * RW, lane, Em1);
+        lds_row<T, V, LP>(tin + 2 * RW, lane, E0);
+        lds_row<T, V, LP>(tin + 3 * RW, lane, E1);
 #pragma unroll
         for (int x = 0; x < V; ++x) Lm[x] = lap_pt(Em1[x + 2], Em1[x + 1], Em1[x + 3], Em2[x + 2], E0[x + 2]);
 #pragma unroll
@@ -404,20 +479,20 @@ __device__ __forceinline__ void hdiff_tile(const double *tin, const double *tcf,
 #pragma unroll
     for (int r = 0; r < JB; ++r) {
         if (!FULL && r >= nrows) break;  // warp-uniform
-        lds_row<V>(tin + (r + 4) * (W + 4), lane, E2);
-        double L1[V + 2], FX[V + 1], FY[V], o[V];
+        lds_row<T, V, LP>(tin + (r + 4) * RW, lane, E2);
+        T L1[V + 2], FX[V + 1], FY[V], o[V];
 #pragma unroll
         for (int y = 0; y < V + 2; ++y) L1[y] = lap_pt(E1[y + 1], E1[y], E1[y + 2], E0[y + 1], E2[y + 1]);
 #pragma unroll
         for (int y = 0; y < V + 1; ++y) FX[y] = limit(Lj[y + 1] - Lj[y], E0[y + 2] - E0[y + 1]);
 #pragma unroll
         for (int x = 0; x < V; ++x) FY[x] = limit(L1[x + 1] - Lj[x + 1], E1[x + 2] - E0[x + 2]);
-        const double *cfr = tcf + r * W + lane * V;
+        const T *cfr = tcf + r * W + lane * V;
 #pragma unroll
         for (int x = 0; x < V; ++x) o[x] = E0[x + 2] - cfr[x] * ((FX[x + 1] - FX[x]) + (FY[x] - FYm[x]));
-        double *op = out_k + (j0 + r) * sj + i_own;
-        if (warp_full) Vec<V>::store(op, o);  // warp-uniform: no per-lane branch
-        else if (own_full) Vec<V>::store(op, o);
+        T *op = out_k + (j0 + r) * sj + i_own;
+        if (warp_full) Vec<T, V>::store(op, o);  // warp-uniform: no per-lane branch
+        else if (own_full) Vec<T, V>::store(op, o);
         else if (own_valid) {
 #pragma unroll
             for (int v = 0; v < V; ++v)
@@ -435,10 +510,10 @@ __device__ __forceinline__ void hdiff_tile(const double *tin, const double *tcf,
     }
 }
 
-template <int V, int JB, int S, int NW>
+template <class T, int V, int JB, int S, int NW>
 __global__ void __launch_bounds__(NW * 32, 1) hdiff_tma(const __grid_constant__ TMap m_in, const __grid_constant__ TMap m_cf,
-                                                     FO out, Dom d, int nseg, int nchunk, int nitems) {
-    using C = TmaCfg<V, JB, S, NW>;
+                                                     FOT<T> out, Dom d, int nseg, int nchunk, int nitems) {
+    using C = TmaCfg<T, V, JB, S, NW>;
     constexpr int W = C::W;
     extern __shared__ __align__(128) unsigned char smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -446,8 +521,8 @@ __global__ void __launch_bounds__(NW * 32, 1) hdiff_tma(const __grid_constant__ 
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem + NW * S * C::SLOT) + warp * S;
     const int gw = blockIdx.x * NW + warp, nwt = gridDim.x * NW;
 
-    auto in_s = [&](int s) { return reinterpret_cast<double *>(wbase + s * C::SLOT); };
-    auto cf_s = [&](int s) { return reinterpret_cast<double *>(wbase + s * C::SLOT + C::IN_PAD); };
+    auto in_s = [&](int s) { return reinterpret_cast<T *>(wbase + s * C::SLOT); };
+    auto cf_s = [&](int s) { return reinterpret_cast<T *>(wbase + s * C::SLOT + C::IN_PAD); };
     auto decode = [&](int item, int &ib, int &j0, int &k) {
         const int seg = item % nseg, chunk = (item / nseg) % nchunk;
         k = d.lo[2] + item / (nseg * nchunk);
@@ -458,7 +533,7 @@ __global__ void __launch_bounds__(NW * 32, 1) hdiff_tma(const __grid_constant__ 
         int ib, j0, k;
         decode(item, ib, j0, k);
         mbar_expect_tx(&bars[s], C::IN_BYTES + C::CF_BYTES);
-        tma_load_ijk(in_s(s), m_in, &bars[s], ib - 2, j0 - 2, k);
+        tma_load_ijk(in_s(s), m_in, &bars[s], ib - C::LP, j0 - 2, k);
         tma_load_ijk(cf_s(s), m_cf, &bars[s], ib, j0, k);
     };
 
@@ -486,13 +561,13 @@ __global__ void __launch_bounds__(NW * 32, 1) hdiff_tma(const __grid_constant__ 
         decode(item, ib, j0, k);
         const int nrows = min(JB, d.hi[1] - j0);
         const int i_own = ib + lane * V;
-        double *out_k = out.p + k * out.sk;
+        T *out_k = out.p + k * out.sk;
         mbar_wait(&bars[s], (n / S) & 1);
         HTRACE(1 + 2 * n);
         if (nrows == JB)
-            hdiff_tile<V, JB, true>(in_s(s), cf_s(s), out_k, out.sj, j0, JB, i_own, d.hi[0], lane);
+            hdiff_tile<T, V, JB, C::LP, true>(in_s(s), cf_s(s), out_k, out.sj, j0, JB, i_own, d.hi[0], lane);
         else
-            hdiff_tile<V, JB, false>(in_s(s), cf_s(s), out_k, out.sj, j0, nrows, i_own, d.hi[0], lane);
+            hdiff_tile<T, V, JB, C::LP, false>(in_s(s), cf_s(s), out_k, out.sj, j0, nrows, i_own, d.hi[0], lane);
         __syncwarp();
         HTRACE(2 + 2 * n);
         if (lane == 0) {
@@ -505,9 +580,9 @@ __global__ void __launch_bounds__(NW * 32, 1) hdiff_tma(const __grid_constant__ 
     }
 }
 
-template <int V, int JB, int S, int NW>
-cudaError_t launch_tma(const TMap &tin, const TMap &tcf, const FO &out, const Dom &d, cudaStream_t st, int *launches) {
-    using C = TmaCfg<V, JB, S, NW>;
+template <class T, int V, int JB, int S, int NW>
+cudaError_t launch_tma(const TMap &tin, const TMap &tcf, const FOT<T> &out, const Dom &d, cudaStream_t st, int *launches) {
+    using C = TmaCfg<T, V, JB, S, NW>;
     const int ni = d.hi[0] - d.lo[0], nj = d.hi[1] - d.lo[1], nk = d.hi[2] - d.lo[2];
     const int nseg = (ni + C::W - 1) / C::W, nchunk = (nj + JB - 1) / JB;
     const long long nitems = (long long)nseg * nchunk * nk;
@@ -515,31 +590,31 @@ cudaError_t launch_tma(const TMap &tin, const TMap &tcf, const FO &out, const Do
     static bool configured = false;
     static int blocks_per_sm = 1, sms = 148;
     if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(hdiff_tma<V, JB, S, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+        cudaError_t e = cudaFuncSetAttribute(hdiff_tma<T, V, JB, S, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
         if (e != cudaSuccess) return e;
         int dev;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, hdiff_tma<V, JB, S, NW>, NW * 32, C::SMEM);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, hdiff_tma<T, V, JB, S, NW>, NW * 32, C::SMEM);
         if (blocks_per_sm < 1) blocks_per_sm = 1;
         configured = true;
     }
     long long blocks = std::min<long long>((nitems + NW - 1) / NW, (long long)sms * blocks_per_sm);
-    cudaError_t e = launch_pdl(hdiff_tma<V, JB, S, NW>, dim3((unsigned)blocks), dim3(NW * 32), C::SMEM, st, tin, tcf, out,
+    cudaError_t e = launch_pdl(hdiff_tma<T, V, JB, S, NW>, dim3((unsigned)blocks), dim3(NW * 32), C::SMEM, st, tin, tcf, out,
                                d, nseg, nchunk, (int)nitems);
     ++*launches;
     return e != cudaSuccess ? e : cudaGetLastError();
 }
 
-template <int V, int JB, int P>
-cudaError_t launch_roll(const FV &in, const FV &coeff, const FO &out, const Dom &d, cudaStream_t s, int *launches) {
+template <class T, int V, int JB, int P>
+cudaError_t launch_roll(const FVT<T> &in, const FVT<T> &coeff, const FOT<T> &out, const Dom &d, cudaStream_t s, int *launches) {
     constexpr int W = 32 * V;
     const int ni = d.hi[0] - d.lo[0], nj = d.hi[1] - d.lo[1], nk = d.hi[2] - d.lo[2];
     const int nseg = (ni + W - 1) / W, nchunk = (nj + JB - 1) / JB;
     const long long warps = (long long)nseg * nchunk * nk;
     const int threads = 128;
     const long long blocks = (warps * 32 + threads - 1) / threads;
-    hdiff_roll<V, JB, P><<<(unsigned)blocks, threads, 0, s>>>(in, coeff, out, d, nseg, nchunk);
+    hdiff_roll<T, V, JB, P><<<(unsigned)blocks, threads, 0, s>>>(in, coeff, out, d, nseg, nchunk);
     ++*launches;
     return cudaGetLastError();
 }
@@ -550,10 +625,28 @@ static bool hdiff_large(const Dom &d) {
     return (long long)(d.hi[0] - d.lo[0]) * (d.hi[1] - d.lo[1]) * (d.hi[2] - d.lo[2]) >= HD_LARGE_POINTS;
 }
 
+// tile configuration per element type: f32 tiles have the same bytes per row as f64 (V doubled)
+template <class T>
+struct HdCfg;
+template <>
+struct HdCfg<double> {
+    static constexpr int V = HD_V, JB = HD_JB, S = HD_S, NW = HD_NW;
+    static constexpr int LV = HDL_V, LJB = HDL_JB, LS = HDL_S, LNW = HDL_NW;
+    static constexpr int RV = 2;  // rolling kernel vector width when 16-byte aligned
+};
+template <>
+struct HdCfg<float> {
+    static constexpr int V = HF_V, JB = HF_JB, S = HF_S, NW = HF_NW;
+    static constexpr int LV = HFL_V, LJB = HFL_JB, LS = HFL_S, LNW = HFL_NW;
+    static constexpr int RV = 4;
+};
+
+template <class T>
 void hdiff_tma_boxes(const Dom &d, int box_in[3], int box_cf[3]) {
+    using C = HdCfg<T>;
     const bool L = hdiff_large(d);
-    const int V = L ? HDL_V : HD_V, JB = L ? HDL_JB : HD_JB;
-    box_in[0] = 32 * V + 4;
+    const int V = L ? C::LV : C::V, JB = L ? C::LJB : C::JB;
+    box_in[0] = 32 * V + 2 * (16 / (int)sizeof(T));  // TmaCfg::RW
     box_in[1] = JB + 4;
     box_in[2] = 1;
     box_cf[0] = 32 * V;
@@ -561,24 +654,34 @@ void hdiff_tma_boxes(const Dom &d, int box_in[3], int box_cf[3]) {
     box_cf[2] = 1;
 }
 
-cudaError_t launch_hdiff(const FV &in, const FV &coeff, const FO &out, const Dom &d, int variant, bool aligned16,
-                         const TMap *tin, const TMap *tcf, cudaStream_t s, int *launches) {
+// aligned16: every field pointer, stride and the domain's i origin allow 16-byte vector accesses
+template <class T>
+cudaError_t launch_hdiff(const FVT<T> &in, const FVT<T> &coeff, const FOT<T> &out, const Dom &d, int variant,
+                         bool aligned16, const TMap *tin, const TMap *tcf, cudaStream_t s, int *launches) {
+    using C = HdCfg<T>;
     if (variant == OEC_VARIANT_NAIVE || variant == OEC_VARIANT_UNROLL2 || variant == OEC_VARIANT_UNROLL4) {
         const int uj = variant == OEC_VARIANT_UNROLL4 ? 4 : variant == OEC_VARIANT_UNROLL2 ? 2 : 1;
         dim3 block(32, 4, 1);
         dim3 grid((d.hi[0] - d.lo[0] + 31) / 32, (d.hi[1] - d.lo[1] + 4 * uj - 1) / (4 * uj), d.hi[2] - d.lo[2]);
-        if (uj == 4) hdiff_naive<4><<<grid, block, 0, s>>>(in, coeff, out, d);
-        else if (uj == 2) hdiff_naive<2><<<grid, block, 0, s>>>(in, coeff, out, d);
-        else hdiff_naive<1><<<grid, block, 0, s>>>(in, coeff, out, d);
+        if (uj == 4) hdiff_naive<T, 4><<<grid, block, 0, s>>>(in, coeff, out, d);
+        else if (uj == 2) hdiff_naive<T, 2><<<grid, block, 0, s>>>(in, coeff, out, d);
+        else hdiff_naive<T, 1><<<grid, block, 0, s>>>(in, coeff, out, d);
         ++*launches;
         return cudaGetLastError();
     }
     if (tin && tcf && aligned16) {
-        if (hdiff_large(d)) return launch_tma<HDL_V, HDL_JB, HDL_S, HDL_NW>(*tin, *tcf, out, d, s, launches);
-        return launch_tma<HD_V, HD_JB, HD_S, HD_NW>(*tin, *tcf, out, d, s, launches);
+        if (hdiff_large(d)) return launch_tma<T, C::LV, C::LJB, C::LS, C::LNW>(*tin, *tcf, out, d, s, launches);
+        return launch_tma<T, C::V, C::JB, C::S, C::NW>(*tin, *tcf, out, d, s, launches);
     }
-    if (aligned16) return launch_roll<2, 16, 4>(in, coeff, out, d, s, launches);
-    return launch_roll<1, 16, 4>(in, coeff, out, d, s, launches);
+    if (aligned16) return launch_roll<T, C::RV, 16, 4>(in, coeff, out, d, s, launches);
+    return launch_roll<T, 1, 16, 4>(in, coeff, out, d, s, launches);
 }
+
+template void hdiff_tma_boxes<double>(const Dom &, int *, int *);
+template void hdiff_tma_boxes<float>(const Dom &, int *, int *);
+template cudaError_t launch_hdiff<double>(const FV &, const FV &, const FO &, const Dom &, int, bool, const TMap *,
+                                          const TMap *, cudaStream_t, int *);
+template cudaError_t launch_hdiff<float>(const FVf &, const FVf &, const FOf &, const Dom &, int, bool, const TMap *,
+                                         const TMap *, cudaStream_t, int *);
 
 }  // namespace oec

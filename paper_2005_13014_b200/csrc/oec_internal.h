@@ -12,47 +12,69 @@ namespace oec {
 // the allocation, only ever dereferenced at validated in-range offsets -- and 32-bit element
 // strides (the host checks every reachable offset fits in int32; "integer index
 // computations are a significant performance bottleneck").
-struct FV {
-    const double *p;
+// T = double (OEC_F64) or float (OEC_F32, the paper's f32 runs).
+template <class T>
+struct FVT {
+    const T *p;
     int32_t sj, sk;  // sk == 0 for k-invariant fields
 };
-struct FO {
-    double *p;
+template <class T>
+struct FOT {
+    T *p;
     int32_t sj, sk;
 };
+using FV = FVT<double>;
+using FO = FOT<double>;
+using FVf = FVT<float>;
+using FOf = FOT<float>;
 
 // Domain of one launch: [lo, hi) in absolute coordinates.
 struct Dom {
     int32_t lo[3], hi[3];
 };
 
-// launchers (return cudaGetLastError() of their launches); `launches` is incremented per launch
-cudaError_t launch_hdiff(const FV &in, const FV &coeff, const FO &out, const Dom &d, int variant, bool aligned16,
-                         const TMap *tin, const TMap *tcf, cudaStream_t s, int *launches);
+// launchers (return cudaGetLastError() of their launches); `launches` is incremented per launch.
+// Templates are instantiated for T = double and T = float; scalars arrive as double and are
+// rounded to T once.
+template <class T>
+cudaError_t launch_hdiff(const FVT<T> &in, const FVT<T> &coeff, const FOT<T> &out, const Dom &d, int variant,
+                         bool aligned16, const TMap *tin, const TMap *tcf, cudaStream_t s, int *launches);
+template <class T>
 void hdiff_tma_boxes(const Dom &d, int box_in[3], int box_cf[3]);
 cudaError_t launch_vadv(const FV &u_stage, const FV &wcon, const FV &u_pos, const FV &utens, const FV &usi,
                         const FO &out, double dtr, const Dom &d, const TMap *tmaps, cudaStream_t s, int *launches);
+// f32 vadv: one thread per column (csrc/vadv.cu vadv_kernel<float>)
+cudaError_t launch_vadv_f32(const FVf &u_stage, const FVf &wcon, const FVf &u_pos, const FVf &utens, const FVf &usi,
+                            const FOf &out, double dtr, const Dom &d, cudaStream_t s, int *launches);
 void vadv_tma_boxes(const Dom &d, int box[3], int box_wc[3], int box_us[3], bool *fits);
 // the paper's "original" level: one kernel per operator, temporaries in HBM (csrc/unfused.cu)
-cudaError_t launch_hdiff_unfused(const FV &in, const FV &coeff, const FO &out, const Dom &d, cudaStream_t s,
-                                 int *launches);
-cudaError_t launch_vadv_unfused(const FV &us, const FV &wc, const FV &up, const FV &ut, const FV &usi, const FO &out,
-                                double dtr, const Dom &d, cudaStream_t s, int *launches);
+template <class T>
+cudaError_t launch_hdiff_unfused(const FVT<T> &in, const FVT<T> &coeff, const FOT<T> &out, const Dom &d,
+                                 cudaStream_t s, int *launches);
+template <class T>
+cudaError_t launch_vadv_unfused(const FVT<T> &us, const FVT<T> &wc, const FVT<T> &up, const FVT<T> &ut,
+                                const FVT<T> &usi, const FOT<T> &out, double dtr, const Dom &d, cudaStream_t s,
+                                int *launches);
 // suite: inputs / outputs in registry order; `unroll` = points per thread along j (1, 2, 4)
-cudaError_t launch_suite(int program_id, const FV *in, const FO *out, const double *scalars, const Dom &d,
+template <class T>
+cudaError_t launch_suite(int program_id, const FVT<T> *in, const FOT<T> *out, const double *scalars, const Dom &d,
                          int unroll, cudaStream_t s, int *launches);
 // suite "original" level: one kernel per stencil.apply, temporaries in HBM (csrc/suite_unfused.cu)
-cudaError_t launch_suite_unfused(int program_id, int n_in, const FV *in, const FO *out, const double *scalars,
-                                 const Dom &d, cudaStream_t s, int *launches);
+template <class T>
+cudaError_t launch_suite_unfused(int program_id, int n_in, const FVT<T> *in, const FOT<T> *out,
+                                 const double *scalars, const Dom &d, cudaStream_t s, int *launches);
 int suite_unfused_stages(int program_id);
 
 // box copies for halo exchange: [lo, hi) box (absolute coords) between fields / packed buffers
 struct Box {
     int32_t lo[3], hi[3];
 };
-cudaError_t launch_pack(const FV &src, const Box &b, double *buf, cudaStream_t s, int *launches);
-cudaError_t launch_unpack(const double *buf, const Box &b, const FO &dst, cudaStream_t s, int *launches);
-cudaError_t launch_box_copy(const FV &src, const FO &dst, const Box &b, cudaStream_t s, int *launches);
+template <class T>
+cudaError_t launch_pack(const FVT<T> &src, const Box &b, T *buf, cudaStream_t s, int *launches);
+template <class T>
+cudaError_t launch_unpack(const T *buf, const Box &b, const FOT<T> &dst, cudaStream_t s, int *launches);
+template <class T>
+cudaError_t launch_box_copy(const FVT<T> &src, const FOT<T> &dst, const Box &b, cudaStream_t s, int *launches);
 
 // error plumbing; launch count reported by oec_last_launch_count
 oec_status set_error(oec_status st, const char *fmt, ...);

@@ -161,6 +161,8 @@ static int find_prog(const char *name) {
 // ---------------------------------------------------------------------------------------------
 // validation
 // ---------------------------------------------------------------------------------------------
+static int esize(int32_t dtype) { return dtype == OEC_F32 ? 4 : 8; }
+
 static bool span_bytes(const oec_field *f, uintptr_t *lo, uintptr_t *hi) {
     // byte range [lo, hi) spanned by the allocation of f
     int64_t mn = 0, mx = 0;
@@ -170,14 +172,19 @@ static bool span_bytes(const oec_field *f, uintptr_t *lo, uintptr_t *hi) {
         int64_t e = (n - 1) * f->stride[d];
         if (e < 0) mn += e; else mx += e;
     }
-    *lo = (uintptr_t)f->data + (uintptr_t)(mn * 8);
-    *hi = (uintptr_t)f->data + (uintptr_t)((mx + 1) * 8);
+    const int es = esize(f->dtype);
+    *lo = (uintptr_t)f->data + (uintptr_t)(mn * es);
+    *hi = (uintptr_t)f->data + (uintptr_t)((mx + 1) * es);
     return true;
 }
 
-static oec_status check_field(const oec_field *f, const char *what, int *device) {
+static oec_status check_field(const oec_field *f, const char *what, int *device, int *dtype) {
     if (!f || !f->data) return set_error(OEC_ERR_ARG, "%s: NULL field or data pointer", what);
-    if (f->dtype != OEC_F64) return set_error(OEC_ERR_DTYPE, "%s: dtype %d is not OEC_F64", what, f->dtype);
+    if (f->dtype != OEC_F64 && f->dtype != OEC_F32)
+        return set_error(OEC_ERR_DTYPE, "%s: dtype %d is neither OEC_F64 nor OEC_F32", what, f->dtype);
+    if (*dtype == -1) *dtype = f->dtype;
+    else if (*dtype != f->dtype)
+        return set_error(OEC_ERR_DTYPE, "%s: dtype %d differs from the other fields' dtype %d", what, f->dtype, *dtype);
     if (*device == -2) *device = f->device;
     else if (*device != f->device)
         return set_error(OEC_ERR_DTYPE, "%s: device %d differs from the other fields' device %d", what, f->device,
@@ -185,7 +192,8 @@ static oec_status check_field(const oec_field *f, const char *what, int *device)
     if (f->stride[0] != 1) return set_error(OEC_ERR_LAYOUT, "%s: stride[0] = %lld, must be 1", what, (long long)f->stride[0]);
     for (int d = 0; d < 3; ++d)
         if (f->ub[d] <= f->lb[d]) return set_error(OEC_ERR_SHAPE, "%s: empty allocation in dim %d", what, d);
-    if (((uintptr_t)f->data) % 8) return set_error(OEC_ERR_LAYOUT, "%s: data not 8-byte aligned", what);
+    if (((uintptr_t)f->data) % esize(f->dtype))
+        return set_error(OEC_ERR_LAYOUT, "%s: data not %d-byte aligned", what, esize(f->dtype));
     return OEC_OK;
 }
 
@@ -207,7 +215,7 @@ static oec_status make_view(const oec_field *f, const char *what, V *v) {
         if (off > INT32_MAX || off < INT32_MIN)
             return set_error(OEC_ERR_LAYOUT, "%s: element offsets exceed int32 (field too large for this build)", what);
     }
-    v->p = (decltype(v->p))((char *)f->data + origin_off * 8);
+    v->p = (decltype(v->p))((char *)f->data + origin_off * (int64_t)sizeof(*v->p));
     v->sj = (int32_t)sj;
     v->sk = (int32_t)sk;
     return OEC_OK;
@@ -276,15 +284,16 @@ static cudaError_t d2h_box(const oec_field *host, const oec_field *dev, const in
     // outer loop over the dimension with the larger stride, 2D copies over the other two
     int outer = (host->stride[2] >= host->stride[1]) ? 2 : 1;
     int mid = 3 - outer;
-    int64_t w = (hi[0] - lo[0]) * 8;
+    const int es = esize(host->dtype);
+    int64_t w = (hi[0] - lo[0]) * es;
     for (int64_t o = lo[outer]; o < hi[outer]; ++o) {
         int64_t idx[3] = {lo[0], 0, 0};
         idx[outer] = o;
         idx[mid] = lo[mid];
         int64_t off = (idx[0] - host->lb[0]) + (idx[1] - host->lb[1]) * host->stride[1] +
                       (is_k_invariant(host) ? 0 : (idx[2] - host->lb[2]) * host->stride[2]);
-        cudaError_t e = cudaMemcpy2DAsync((char *)host->data + off * 8, host->stride[mid] * 8,
-                                          (char *)dev->data + off * 8, dev->stride[mid] * 8, w, hi[mid] - lo[mid],
+        cudaError_t e = cudaMemcpy2DAsync((char *)host->data + off * es, host->stride[mid] * es,
+                                          (char *)dev->data + off * es, dev->stride[mid] * es, w, hi[mid] - lo[mid],
                                           cudaMemcpyDeviceToHost, s);
         if (e != cudaSuccess) return e;
     }
@@ -302,35 +311,37 @@ static int unroll_of(int p, int variant) {
     return variant == OEC_VARIANT_UNROLL2 ? 2 : variant == OEC_VARIANT_UNROLL4 ? 4 : 1;
 }
 
+template <class T>
 static oec_status run_device(int p, const oec_field *const *in, oec_field *const *out, const double *sc,
                              const int64_t *lo, const int64_t *hi, int variant, cudaStream_t s) {
     const ProgSpec &P = PROGS[p];
-    FV v_in[9];
-    FO v_out[3];
+    FVT<T> v_in[9];
+    FOT<T> v_out[3];
+    constexpr int V16 = 16 / (int)sizeof(T);  // elements per 16 bytes
     bool aligned16 = true;
     for (int q = 0; q < P.n_in; ++q) {
         oec_status st = make_view(in[q], P.in[q].name, &v_in[q]);
         if (st) return st;
-        aligned16 = aligned16 && ((uintptr_t)v_in[q].p % 16 == 0) && (v_in[q].sj % 2 == 0) && (v_in[q].sk % 2 == 0);
+        aligned16 = aligned16 && ((uintptr_t)v_in[q].p % 16 == 0) && (v_in[q].sj % V16 == 0) && (v_in[q].sk % V16 == 0);
     }
     for (int q = 0; q < P.n_out; ++q) {
         oec_status st = make_view(out[q], P.out[q], &v_out[q]);
         if (st) return st;
-        aligned16 = aligned16 && ((uintptr_t)v_out[q].p % 16 == 0) && (v_out[q].sj % 2 == 0) && (v_out[q].sk % 2 == 0);
+        aligned16 = aligned16 && ((uintptr_t)v_out[q].p % 16 == 0) && (v_out[q].sj % V16 == 0) && (v_out[q].sk % V16 == 0);
     }
     Dom d;
     for (int q = 0; q < 3; ++q) {
         d.lo[q] = (int32_t)lo[q];
         d.hi[q] = (int32_t)hi[q];
     }
-    aligned16 = aligned16 && (d.lo[0] % 2 == 0);
+    aligned16 = aligned16 && (d.lo[0] % V16 == 0);
     int launches = 0;
     cudaError_t e;
     if (variant == OEC_VARIANT_UNFUSED) {
-        if (p == OEC_PROG_HDIFF) e = launch_hdiff_unfused(v_in[0], v_in[1], v_out[0], d, s, &launches);
+        if (p == OEC_PROG_HDIFF) e = launch_hdiff_unfused<T>(v_in[0], v_in[1], v_out[0], d, s, &launches);
         else if (p == OEC_PROG_VADV)
-            e = launch_vadv_unfused(v_in[0], v_in[1], v_in[2], v_in[3], v_in[4], v_out[0], sc[0], d, s, &launches);
-        else e = launch_suite_unfused(p, P.n_in, v_in, v_out, sc, d, s, &launches);
+            e = launch_vadv_unfused<T>(v_in[0], v_in[1], v_in[2], v_in[3], v_in[4], v_out[0], sc[0], d, s, &launches);
+        else e = launch_suite_unfused<T>(p, P.n_in, v_in, v_out, sc, d, s, &launches);
         if (e != cudaSuccess) return set_error(OEC_ERR_CUDA, "%s (unfused): %s", P.name, cudaGetErrorString(e));
         g_launches = launches;
         return OEC_OK;
@@ -339,25 +350,29 @@ static oec_status run_device(int p, const oec_field *const *in, oec_field *const
     case OEC_PROG_HDIFF: {
         TMap tin, tcf;
         int bin[3], bcf[3];
-        hdiff_tma_boxes(d, bin, bcf);
+        hdiff_tma_boxes<T>(d, bin, bcf);
         const bool tma = variant == OEC_VARIANT_AUTO && make_tmap(in[0], bin, &tin) && make_tmap(in[1], bcf, &tcf);
-        e = launch_hdiff(v_in[0], v_in[1], v_out[0], d, variant, aligned16, tma ? &tin : nullptr, tma ? &tcf : nullptr,
+        e = launch_hdiff<T>(v_in[0], v_in[1], v_out[0], d, variant, aligned16, tma ? &tin : nullptr, tma ? &tcf : nullptr,
                          s, &launches);
         break;
     }
     case OEC_PROG_VADV: {
-        // TMA path: u_stage, wcon, u_pos, utens, utens_stage_in (tmaps[0..4])
-        TMap tm[5];
-        int box[3], bwc[3], bus[3];
-        bool fits;
-        vadv_tma_boxes(d, box, bwc, bus, &fits);
-        bool tma = fits && aligned16 && variant == OEC_VARIANT_AUTO;
-        for (int q = 0; q < 5 && tma; ++q) tma = make_tmap(in[q], q == 0 ? bus : (q == 1 ? bwc : box), &tm[q]);
-        e = launch_vadv(v_in[0], v_in[1], v_in[2], v_in[3], v_in[4], v_out[0], sc[0], d, tma ? tm : nullptr, s,
-                        &launches);
+        if constexpr (sizeof(T) == 4) {  // f32: one thread per column (all variants but UNFUSED)
+            e = launch_vadv_f32(v_in[0], v_in[1], v_in[2], v_in[3], v_in[4], v_out[0], sc[0], d, s, &launches);
+        } else {
+            // TMA path: u_stage, wcon, u_pos, utens, utens_stage_in (tmaps[0..4])
+            TMap tm[5];
+            int box[3], bwc[3], bus[3];
+            bool fits;
+            vadv_tma_boxes(d, box, bwc, bus, &fits);
+            bool tma = fits && aligned16 && variant == OEC_VARIANT_AUTO;
+            for (int q = 0; q < 5 && tma; ++q) tma = make_tmap(in[q], q == 0 ? bus : (q == 1 ? bwc : box), &tm[q]);
+            e = launch_vadv(v_in[0], v_in[1], v_in[2], v_in[3], v_in[4], v_out[0], sc[0], d, tma ? tm : nullptr, s,
+                            &launches);
+        }
         break;
     }
-    default: e = launch_suite(p, v_in, v_out, sc, d, unroll_of(p, variant), s, &launches); break;
+    default: e = launch_suite<T>(p, v_in, v_out, sc, d, unroll_of(p, variant), s, &launches); break;
     }
     if (e != cudaSuccess) return set_error(OEC_ERR_CUDA, "%s: kernel launch failed: %s", P.name, cudaGetErrorString(e));
     g_launches = launches;
@@ -383,11 +398,12 @@ static oec_status apply(int p, const oec_field *const *in, int n_in, oec_field *
                          "no shared producers for CSE to remove)");
     oec_status st = check_domain(lo, hi);
     if (st) return st;
-    int device = -2;
+    int device = -2, dtype = -1;
     for (int q = 0; q < P.n_in; ++q)
-        if ((st = check_field(in[q], P.in[q].name, &device))) return st;
+        if ((st = check_field(in[q], P.in[q].name, &device, &dtype))) return st;
     for (int q = 0; q < P.n_out; ++q)
-        if ((st = check_field(out[q], P.out[q], &device))) return st;
+        if ((st = check_field(out[q], P.out[q], &device, &dtype))) return st;
+    auto run = dtype == OEC_F32 ? run_device<float> : run_device<double>;
     for (int q = 0; q < P.n_out; ++q)
         if (is_k_invariant(out[q]))
             return set_error(OEC_ERR_SHAPE, "%s: output %s must not be k-invariant", P.name, P.out[q]);
@@ -424,7 +440,7 @@ static oec_status apply(int p, const oec_field *const *in, int n_in, oec_field *
     if (empty) return OEC_OK;
     cudaStream_t s = (cudaStream_t)stream;
 
-    if (device >= 0) return run_device(p, in, out, sc, lo, hi, variant, s);
+    if (device >= 0) return run(p, in, out, sc, lo, hi, variant, s);
     if (device != OEC_DEVICE_HOST) return set_error(OEC_ERR_ARG, "%s: invalid device %d", P.name, device);
 
     // ---- end-to-end path: stage host fields through cached device buffers ----
@@ -455,7 +471,7 @@ static oec_status apply(int p, const oec_field *const *in, int n_in, oec_field *
         dout[q].data = (char *)dptr + ((uintptr_t)out[q]->data - b0);
         pout[q] = &dout[q];
     }
-    if ((st = run_device(p, pin, pout, sc, lo, hi, variant, s))) return st;
+    if ((st = run(p, pin, pout, sc, lo, hi, variant, s))) return st;
     int launches = g_launches;
     for (int q = 0; q < P.n_out; ++q) {
         cudaError_t e = d2h_box(out[q], &dout[q], lo, hi, s);
@@ -476,8 +492,9 @@ extern "C" {
 int32_t oec_abi_version(void) { return OEC_ABI_VERSION; }
 
 const char *oec_build_info(void) {
-    return "liboec: sm_100a, fp64, --fmad=false, kernels: hdiff(rolling-j register/shuffle, naive), vadv(thomas, "
-           "register-prefetch, smem c'/d'), suite(inlined per-point), halo(pack/unpack, NCCL send/recv)";
+    return "liboec: sm_100a, fp64 + f32, --fmad=false; kernels: hdiff (TMA ring, rolling-j, naive/unrolled, unfused), "
+           "vadv (TMEM c'/d' specialised, TMA smem, one thread per column, unfused), suite (inlined per point, "
+           "unrolled along j, unfused per operator), halo (pack/unpack, NCCL send/recv)";
 }
 
 const char *oec_last_error(void) { return g_err; }
@@ -488,12 +505,14 @@ oec_status oec_field_create(const int64_t domain[3], const int32_t halo_lo[3], c
                             int32_t device, const int32_t order[3], int32_t k_invariant, oec_field *out) {
     g_err[0] = 0;
     if (!domain || !halo_lo || !halo_hi || !out) return set_error(OEC_ERR_ARG, "oec_field_create: NULL argument");
-    if (dtype != OEC_F64) return set_error(OEC_ERR_DTYPE, "oec_field_create: dtype %d unsupported", dtype);
+    if (dtype != OEC_F64 && dtype != OEC_F32) return set_error(OEC_ERR_DTYPE, "oec_field_create: dtype %d unsupported", dtype);
+    const int es = esize(dtype), pad = 128 / es;  // i = 0 is 128-byte aligned; pitch 128-byte multiple
     if (device < 0) return set_error(OEC_ERR_ARG, "oec_field_create: device %d must be a CUDA ordinal", device);
     for (int d = 0; d < 3; ++d)
         if (domain[d] < 1 || halo_lo[d] < 0 || halo_hi[d] < 0)
             return set_error(OEC_ERR_ARG, "oec_field_create: domain >= 1 and halos >= 0 required");
-    if (halo_lo[0] > 16) return set_error(OEC_ERR_ARG, "oec_field_create: i halo_lo %d > 16 (the left pad)", halo_lo[0]);
+    if (halo_lo[0] > pad)
+        return set_error(OEC_ERR_ARG, "oec_field_create: i halo_lo %d > %d (the left pad)", halo_lo[0], pad);
     if (k_invariant && (domain[2] != 1 || halo_lo[2] || halo_hi[2]))
         return set_error(OEC_ERR_ARG, "oec_field_create: k_invariant requires domain[2] == 1 and no k halo");
     int ord[3] = {0, 2, 1};
@@ -507,17 +526,17 @@ oec_status oec_field_create(const int64_t domain[3], const int32_t halo_lo[3], c
         }
         if (ord[0] != 0) return set_error(OEC_ERR_LAYOUT, "oec_field_create: i must be the fastest dimension");
     }
-    // i: 16-element left pad (i = 0 is 128-byte aligned), pitch a multiple of 16 elements
+    // i: 128-byte left pad (i = 0 is 128-byte aligned), pitch a multiple of 128 bytes
     int64_t n[3];
-    n[0] = 16 + domain[0] + halo_hi[0];
-    n[0] = (n[0] + 15) / 16 * 16;
+    n[0] = pad + domain[0] + halo_hi[0];
+    n[0] = (n[0] + pad - 1) / pad * pad;
     n[1] = domain[1] + halo_lo[1] + halo_hi[1];
     n[2] = domain[2] + halo_lo[2] + halo_hi[2];
     int64_t stride[3];
     stride[ord[0]] = 1;
     stride[ord[1]] = n[ord[0]];
     stride[ord[2]] = n[ord[0]] * n[ord[1]];
-    size_t bytes = (size_t)(n[0] * n[1] * n[2]) * 8;
+    size_t bytes = (size_t)(n[0] * n[1] * n[2]) * es;
     int prev;
     cudaGetDevice(&prev);
     cudaSetDevice(device);
@@ -536,8 +555,8 @@ oec_status oec_field_create(const int64_t domain[3], const int32_t halo_lo[3], c
     out->stride[0] = 1;
     out->stride[1] = stride[1];
     out->stride[2] = k_invariant ? 0 : stride[2];
-    // data points at (lb0, lb1, lb2): the row starts 16 - halo_lo[0] elements into the pad
-    out->data = (char *)base + (16 - halo_lo[0]) * 8;
+    // data points at (lb0, lb1, lb2): the row starts pad - halo_lo[0] elements into the pad
+    out->data = (char *)base + (pad - halo_lo[0]) * es;
     out->dtype = dtype;
     out->device = device;
     out->owned = 1;
@@ -548,7 +567,7 @@ oec_status oec_field_wrap(void *data, const int64_t lb[3], const int64_t ub[3], 
                           int32_t device, oec_field *out) {
     g_err[0] = 0;
     if (!data || !lb || !ub || !stride || !out) return set_error(OEC_ERR_ARG, "oec_field_wrap: NULL argument");
-    if (dtype != OEC_F64) return set_error(OEC_ERR_DTYPE, "oec_field_wrap: dtype %d unsupported", dtype);
+    if (dtype != OEC_F64 && dtype != OEC_F32) return set_error(OEC_ERR_DTYPE, "oec_field_wrap: dtype %d unsupported", dtype);
     if (stride[0] != 1) return set_error(OEC_ERR_LAYOUT, "oec_field_wrap: stride[0] must be 1");
     for (int d = 0; d < 3; ++d)
         if (ub[d] <= lb[d]) return set_error(OEC_ERR_ARG, "oec_field_wrap: empty range in dim %d", d);
@@ -571,7 +590,8 @@ oec_status oec_field_destroy(oec_field *f) {
     g_err[0] = 0;
     if (!f) return set_error(OEC_ERR_ARG, "oec_field_destroy: NULL");
     if (f->owned && f->data) {
-        void *base = (char *)f->data - (16 + f->lb[0]) * 8;
+        const int es = esize(f->dtype), pad = 128 / es;
+        void *base = (char *)f->data - (pad + f->lb[0]) * es;
         int prev;
         cudaGetDevice(&prev);
         cudaSetDevice(f->device);

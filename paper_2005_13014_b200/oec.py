@@ -22,6 +22,7 @@ LIB_PATH = os.environ.get("OEC_LIB_PATH") or os.path.join(_HERE, "liboec.so")
 OEC_OK = 0
 OEC_DEVICE_HOST = -1
 OEC_F64 = 0
+OEC_F32 = 1
 OEC_VARIANT_AUTO = 0
 OEC_VARIANT_UNFUSED = 1
 OEC_VARIANT_NAIVE = 2
@@ -145,11 +146,11 @@ def _stream(stream) -> Optional[int]:
 class _CudaArray:
     """__cuda_array_interface__ over a field's allocation, for zero-copy torch views."""
 
-    def __init__(self, ptr: int, shape, strides_bytes, keep):
+    def __init__(self, ptr: int, shape, strides_bytes, keep, typestr="<f8"):
         self.__cuda_array_interface__ = {
             "shape": tuple(shape),
             "strides": tuple(strides_bytes),
-            "typestr": "<f8",
+            "typestr": typestr,
             "data": (ptr, False),
             "version": 3,
         }
@@ -180,6 +181,14 @@ class Field:
         return self.desc.device
 
     @property
+    def dtype(self) -> int:
+        return self.desc.dtype
+
+    @property
+    def itemsize(self) -> int:
+        return 4 if self.desc.dtype == OEC_F32 else 8
+
+    @property
     def ptr(self):
         return C.pointer(self.desc)
 
@@ -191,7 +200,9 @@ class Field:
             return torch.from_numpy(self._keep) if isinstance(self._keep, np.ndarray) else self._keep
         n = [self.desc.ub[d] - self.desc.lb[d] for d in range(3)]
         st = self.desc.stride
-        arr = _CudaArray(self.desc.data, (n[2], n[1], n[0]), (st[2] * 8, st[1] * 8, st[0] * 8), self)
+        es = self.itemsize
+        arr = _CudaArray(self.desc.data, (n[2], n[1], n[0]), (st[2] * es, st[1] * es, st[0] * es), self,
+                         "<f4" if es == 4 else "<f8")
         return torch.as_tensor(arr, device=f"cuda:{self.desc.device}")
 
     def upload(self, host) -> "Field":
@@ -224,11 +235,28 @@ class Field:
 # ---------------------------------------------------------------------------------------------
 # fields
 # ---------------------------------------------------------------------------------------------
+def _dtype_code(dtype) -> int:
+    """numpy / torch dtype (or an OEC_F* code) -> oec_dtype."""
+    if isinstance(dtype, int):
+        return dtype
+    name = str(dtype).replace("torch.", "")
+    if not name.startswith("float") and name not in ("double", "<f8", "<f4"):
+        try:
+            name = np.dtype(dtype).name  # numpy scalar types, np.dtype objects, strings like "f4"
+        except TypeError:
+            pass
+    if name in ("float64", "double", "<f8"):
+        return OEC_F64
+    if name in ("float32", "float", "<f4"):
+        return OEC_F32
+    raise ValueError(f"unsupported dtype {dtype!r} (fp64 or f32)")
+
+
 def oec_field_create(domain, halo_lo=(0, 0, 0), halo_hi=(0, 0, 0), device: int = 0, order=None,
-                     k_invariant: bool = False) -> Field:
+                     k_invariant: bool = False, dtype=OEC_F64) -> Field:
     d = OecField()
     order_arg = _i32(order) if order is not None else None
-    _check(lib().oec_field_create(_i64(domain), _i32(halo_lo), _i32(halo_hi), OEC_F64, device, order_arg,
+    _check(lib().oec_field_create(_i64(domain), _i32(halo_lo), _i32(halo_hi), _dtype_code(dtype), device, order_arg,
                                   int(k_invariant), C.byref(d)))
     return Field(d)
 
@@ -240,13 +268,13 @@ def oec_field_wrap(array, lb, ub, stride=None, device: Optional[int] = None, k_i
     import torch
 
     d = OecField()
+    dt = _dtype_code(array.dtype)
     if isinstance(array, np.ndarray):
-        assert array.dtype == np.float64
+        es = array.itemsize
         ptr = array.ctypes.data
-        st = stride or (array.strides[2] // 8, array.strides[1] // 8, array.strides[0] // 8)
+        st = stride or (array.strides[2] // es, array.strides[1] // es, array.strides[0] // es)
         dev = OEC_DEVICE_HOST
     else:
-        assert array.dtype == torch.float64
         ptr = array.data_ptr()
         st = stride or (array.stride(2), array.stride(1), array.stride(0))
         dev = array.device.index if array.is_cuda else OEC_DEVICE_HOST
@@ -257,7 +285,7 @@ def oec_field_wrap(array, lb, ub, stride=None, device: Optional[int] = None, k_i
     st = list(st)
     if k_invariant:
         st[2] = 0
-    _check(lib().oec_field_wrap(C.c_void_p(ptr), _i64(lb), _i64(ub), _i64(st), OEC_F64, dev, C.byref(d)))
+    _check(lib().oec_field_wrap(C.c_void_p(ptr), _i64(lb), _i64(ub), _i64(st), dt, dev, C.byref(d)))
     return Field(d, keep=array)
 
 
@@ -268,12 +296,14 @@ def field_from_host(host, device: int = 0, order=None) -> Field:
     lb, ub, kinv = host.lb, host.ub, getattr(host, "k_invariant", False)
     if any(lb[d] > 0 for d in range(3)) or any(ub[d] < 1 for d in range(3)):
         raise ValueError("field_from_host: allocation must contain the origin")
-    f = oec_field_create(ub, [-x for x in lb], (0, 0, 0), device=device, order=order, k_invariant=kinv)
+    data = getattr(host, "data", host)
+    f = oec_field_create(ub, [-x for x in lb], (0, 0, 0), device=device, order=order, k_invariant=kinv,
+                         dtype=data.dtype)
     return f.upload(host)
 
 
-def empty_like_domain(domain, device: int = 0, order=None, fill: float = float("nan")) -> Field:
-    f = oec_field_create(domain, (0, 0, 0), (0, 0, 0), device=device, order=order)
+def empty_like_domain(domain, device: int = 0, order=None, fill: float = float("nan"), dtype=OEC_F64) -> Field:
+    f = oec_field_create(domain, (0, 0, 0), (0, 0, 0), device=device, order=order, dtype=dtype)
     return f.fill(fill)
 
 

@@ -24,7 +24,8 @@ def run_gpu(program, host, domain, order=None, dom_lb=(0, 0, 0), dom_ub=None, va
     dom_ub = dom_ub or domain
     spec = synth.PROGRAMS[program]
     ins = [oec.field_from_host(host[s.name], order=order) for s in spec.inputs]
-    outs = [oec.oec_field_create(domain, out_halo, out_halo, order=order).fill(SENTINEL) for _ in spec.outputs]
+    dt = host[spec.inputs[0].name].data.dtype
+    outs = [oec.oec_field_create(domain, out_halo, out_halo, order=order, dtype=dt).fill(SENTINEL) for _ in spec.outputs]
     sc = scalars if scalars is not None else [v for _, v in spec.scalars]
     oec.oec_apply_program(program, ins, outs, sc, dom_lb, dom_ub, variant, stream)
     torch.cuda.synchronize()
@@ -40,12 +41,13 @@ def run_oracle(program, host, domain, dom_lb=(0, 0, 0), dom_ub=None, scalars=Non
     ni, nj, nk = (dom_ub[d] - dom_lb[d] for d in range(3))
     spec = synth.PROGRAMS[program]
     sc = dict(zip([n for n, _ in spec.scalars], scalars)) if scalars is not None else synth.scalars(program)
+    dt = host[spec.inputs[0].name].data.dtype
     if program == "hdiff":
-        o = HostField(np.full((nk, nj, ni), np.nan), tuple(dom_lb), tuple(dom_ub))
+        o = HostField(np.full((nk, nj, ni), np.nan, dtype=dt), tuple(dom_lb), tuple(dom_ub))
         capi.hdiff(host["in"], host["coeff"], o, dom_lb, dom_ub, capi.HDIFF_UNFUSED, nthreads)
         return {"out": o.data}
     if program == "vadv":
-        o = HostField(np.full((nk, nj, ni), np.nan), tuple(dom_lb), tuple(dom_ub))
+        o = HostField(np.full((nk, nj, ni), np.nan, dtype=dt), tuple(dom_lb), tuple(dom_ub))
         capi.vadv(host, o, sc["dtr_stage"], dom_lb, dom_ub, capi.VADV_UNFUSED, nthreads)
         return {"utens_stage_out": o.data}
     r = st.run_unfused(suite.PROGRAMS[program], host, sc, dom_lb, dom_ub)
@@ -70,5 +72,7 @@ def compare(gpu: np.ndarray, ref: np.ndarray):
     rel = np.max(np.abs(gpu[nz] - ref[nz]) / np.abs(ref[nz])) if nz.any() else 0.0
     zero_ok = np.all(gpu[~nz] == 0) if (~nz).any() else True
     norm = np.max(np.abs(gpu - ref)) / max(np.max(np.abs(ref)), 1e-300)
-    nbits = int(np.sum(gpu.view(np.uint64) != ref.view(np.uint64)))
+    assert gpu.dtype == ref.dtype, (gpu.dtype, ref.dtype)
+    u = np.uint64 if gpu.dtype.itemsize == 8 else np.uint32
+    nbits = int(np.sum(gpu.view(u) != ref.view(u)))
     return dict(max_rel=float(rel), zero_ok=bool(zero_ok), normwise=float(norm), n_bitdiff=nbits, n=gpu.size)

@@ -137,6 +137,16 @@ def test_error_vadv_k1():
     assert stt == 2 and "K = 1" in msg
 
 
+def test_error_mixed_dtypes():
+    inp, cf, out = _hdiff_host_fields()
+    o32 = oec.oec_field_wrap(np.zeros((2, 8, 8), np.float32), (0, 0, 0), (8, 8, 2))
+    stt, msg = _status(lambda: oec.oec_hdiff(inp, cf, o32, (0, 0, 0), (8, 8, 2)))
+    assert stt == 4 and "dtype" in msg
+    bad = oec.oec_field_wrap(np.zeros((2, 8, 8), np.float32), (0, 0, 0), (8, 8, 2))
+    bad.desc.dtype = 7
+    assert _status(lambda: oec.oec_hdiff(inp, cf, bad, (0, 0, 0), (8, 8, 2)))[0] == 4
+
+
 def test_error_mixed_devices():
     inp, cf, out = _hdiff_host_fields()
     out.desc.device = 0

@@ -17,13 +17,14 @@ pytestmark = pytest.mark.gpu
     ("hdiff", (129, 40, 4), 4, 2, ((2, 2, 0), (2, 2, 0))),
     ("vadv", (130, 20, 12), 2, 1, ((0, 0, 0), (1, 0, 0))),
 ])
-def test_local_exchange_matches_global(program, gdom, px, py, w):
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_local_exchange_matches_global(program, gdom, px, py, w, dtype):
     import torch
 
     from paper_2005_13014_b200 import oec
 
     wlo, whi = w
-    host = synth.make_inputs(program, gdom, seed=9)
+    host = synth.make_inputs(program, gdom, seed=9, dtype=dtype)
     spec = synth.PROGRAMS[program]
     R = px * py
     decs = [oec.oec_decomp_create(gdom, px, py, r) for r in range(R)]
@@ -35,7 +36,7 @@ def test_local_exchange_matches_global(program, gdom, px, py, w):
         rank_fields = {}
         for s in spec.inputs:
             g = host[s.name]
-            f = oec.oec_field_create(ldom, s.halo_lo, s.halo_hi)
+            f = oec.oec_field_create(ldom, s.halo_lo, s.halo_hi, dtype=dtype)
             v = f.view()  # [k][j][i] over the local allocation
             v.fill_(float("nan"))
             # own interior + global outer halo (caller data) from the global field
@@ -55,7 +56,7 @@ def test_local_exchange_matches_global(program, gdom, px, py, w):
     sc = [v for _, v in spec.scalars]
     for r, dec in enumerate(decs):
         ldom = tuple(dec.local_ub[d] - dec.local_lb[d] for d in range(3))
-        out = oec.empty_like_domain(ldom)
+        out = oec.empty_like_domain(ldom, dtype=dtype)
         oec.oec_apply_program(program, [fields[r][s.name] for s in spec.inputs], [out], sc, (0, 0, 0), ldom)
         outs.append(out)
     torch.cuda.synchronize()
