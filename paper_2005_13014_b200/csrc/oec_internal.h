@@ -43,9 +43,11 @@ template <class T>
 void hdiff_tma_boxes(const Dom &d, int box_in[3], int box_cf[3]);
 cudaError_t launch_vadv(const FV &u_stage, const FV &wcon, const FV &u_pos, const FV &utens, const FV &usi,
                         const FO &out, double dtr, const Dom &d, const TMap *tmaps, cudaStream_t s, int *launches);
-// f32 vadv: one thread per column (csrc/vadv.cu vadv_kernel<float>)
+// f32 vadv: the TMA / shared-memory solver (vadv_tma<float>) when tmaps is given, else one thread
+// per column (vadv_kernel<float>)
 cudaError_t launch_vadv_f32(const FVf &u_stage, const FVf &wcon, const FVf &u_pos, const FVf &utens, const FVf &usi,
-                            const FOf &out, double dtr, const Dom &d, cudaStream_t s, int *launches);
+                            const FOf &out, double dtr, const Dom &d, const TMap *tmaps, cudaStream_t s, int *launches);
+template <class T>
 void vadv_tma_boxes(const Dom &d, int box[3], int box_wc[3], int box_us[3], bool *fits);
 // the paper's "original" level: one kernel per operator, temporaries in HBM (csrc/unfused.cu)
 template <class T>

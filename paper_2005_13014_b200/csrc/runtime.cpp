@@ -357,19 +357,19 @@ static oec_status run_device(int p, const oec_field *const *in, oec_field *const
         break;
     }
     case OEC_PROG_VADV: {
-        if constexpr (sizeof(T) == 4) {  // f32: one thread per column (all variants but UNFUSED)
-            e = launch_vadv_f32(v_in[0], v_in[1], v_in[2], v_in[3], v_in[4], v_out[0], sc[0], d, s, &launches);
-        } else {
-            // TMA path: u_stage, wcon, u_pos, utens, utens_stage_in (tmaps[0..4])
-            TMap tm[5];
-            int box[3], bwc[3], bus[3];
-            bool fits;
-            vadv_tma_boxes(d, box, bwc, bus, &fits);
-            bool tma = fits && aligned16 && variant == OEC_VARIANT_AUTO;
-            for (int q = 0; q < 5 && tma; ++q) tma = make_tmap(in[q], q == 0 ? bus : (q == 1 ? bwc : box), &tm[q]);
+        // TMA path: u_stage, wcon, u_pos, utens, utens_stage_in (tmaps[0..4])
+        TMap tm[5];
+        int box[3], bwc[3], bus[3];
+        bool fits;
+        vadv_tma_boxes<T>(d, box, bwc, bus, &fits);
+        bool tma = fits && aligned16 && variant == OEC_VARIANT_AUTO;
+        for (int q = 0; q < 5 && tma; ++q) tma = make_tmap(in[q], q == 0 ? bus : (q == 1 ? bwc : box), &tm[q]);
+        if constexpr (sizeof(T) == 4)
+            e = launch_vadv_f32(v_in[0], v_in[1], v_in[2], v_in[3], v_in[4], v_out[0], sc[0], d, tma ? tm : nullptr, s,
+                                &launches);
+        else
             e = launch_vadv(v_in[0], v_in[1], v_in[2], v_in[3], v_in[4], v_out[0], sc[0], d, tma ? tm : nullptr, s,
                             &launches);
-        }
         break;
     }
     default: e = launch_suite<T>(p, v_in, v_out, sc, d, unroll_of(p, variant), s, &launches); break;

@@ -23,6 +23,7 @@ def main():
     ap.add_argument("--variant", type=int, default=0)
     ap.add_argument("--reps", type=int, default=30)
     ap.add_argument("--tag", default="")
+    ap.add_argument("--dtype", default="f64", choices=["f64", "f32"])
     a = ap.parse_args()
     import torch
 
@@ -52,16 +53,19 @@ def main():
             print(json.dumps({"tag": a.tag, "program": "copy16MiB", "us": round(us, 3),
                               "GB/s": round(2 * n * 8 / (us * 1e-6) / 1e9, 1)}), flush=True)
             continue
-        host = synth.make_inputs(program, dom, seed=0)
+        import numpy as np
+
+        dt = np.float32 if a.dtype == "f32" else np.float64
+        host = synth.make_inputs(program, dom, seed=0, dtype=dt)
         spec = synth.PROGRAMS[program]
         sc = [v for _, v in spec.scalars]
 
         def make():
             return ([oec.field_from_host(host[s.name]) for s in spec.inputs],
-                    [oec.empty_like_domain(dom, fill=0.0) for _ in spec.outputs])
+                    [oec.empty_like_domain(dom, fill=0.0, dtype=dt) for _ in spec.outputs])
 
         s0 = make()
-        nb = sum(int(math.prod([f.ub[d] - f.lb[d] for d in range(3)])) * 8 for f in s0[0] + s0[1])
+        nb = sum(int(math.prod([f.ub[d] - f.lb[d] for d in range(3)])) * f.itemsize for f in s0[0] + s0[1])
         R = max(2, math.ceil(4 * l2 / nb) + 1)
         sets = [s0] + [make() for _ in range(R - 1)]
         for ins, outs in sets:
@@ -80,9 +84,9 @@ def main():
         e1.record()
         torch.cuda.synchronize()
         us = 1e3 * e0.elapsed_time(e1) / (a.reps * R)
-        nbytes = program_bytes(program, dom)
+        nbytes = program_bytes(program, dom) * np.dtype(dt).itemsize // 8
         gbs = nbytes / (us * 1e-6) / 1e9
-        print(json.dumps({"tag": a.tag, "program": program, "domain": dom, "variant": a.variant, "us": round(us, 3),
+        print(json.dumps({"tag": a.tag, "program": program, "domain": dom, "variant": a.variant, "dtype": a.dtype, "us": round(us, 3),
                           "GB/s": round(gbs, 1), "frac": round(gbs / peak, 4), "sets": R}), flush=True)
         del sets, s0, g
 
