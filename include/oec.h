@@ -248,6 +248,71 @@ oec_status oec_halo_exchange_local(const int64_t global_domain[3], int32_t px, i
 oec_status oec_decomp_destroy(oec_decomp *d);
 
 /* ----------------------------------------------------------------------------------------- */
+/* Multi-step hdiff with the halo exchange fused into the kernel (SURVEY §8(f) rank 2;         */
+/* north_star (3): "halo exchange via NCCL or P2P over NVLink overlapped with interior          */
+/* compute").  Not in PAPER.md (single GPU, one application per run).                          */
+/* ----------------------------------------------------------------------------------------- */
+/* A pipeline advances x_{t+1} = hdiff(x_t, coeff) on one rank's sub-domain of a px x py
+ * decomposition (oec_decomp_create's split) for any number of steps without host round trips:
+ * x_t lives in x0 (t even) or x1 (t odd).  Each step is ONE kernel: tiles whose 13-point diamond
+ * stays inside the sub-domain stream through the TMA ring first; the boundary tiles then read
+ * the neighbours' cells of x_t directly from the neighbours' x0/x1 (device pointers valid on this
+ * device: NVLink peer memory imported with oec_ipc_import, or plain pointers when the sub-domains
+ * share a device), after the neighbours have signalled (st.release.sys into this rank's signal
+ * pad) that step t-1 is complete.  No halo is copied and there is no exchange launch; the
+ * transfer overlaps the interior tiles.  The step counter t lives in device memory, so a CUDA
+ * graph of captured oec_hdiff_pipeline_run calls advances on every replay.
+ *
+ * Semantics (R19, R23): the global domain is non-periodic; cells outside it are the
+ * caller's global outer halo, which is CONSTANT over the steps: x0 and x1 must hold the same
+ * values there (e.g. x1 created as a copy of x0).  After n steps the result equals n
+ * applications of oec_hdiff on the global domain, each followed by copying the outer halo of x0
+ * into the new field -- bit for bit.
+ *
+ * Fields, in the rank's LOCAL coordinates (origin = local_lb of oec_decomp_create):
+ *   x0, x1   device fields covering the sub-domain grown by 2 in i and j (all of k); identical
+ *            lb/ub/strides; TMA-describable (oec_field_create layout); x0, x1, coeff alias-free
+ *   coeff    covers the sub-domain
+ * Every sub-domain must be >= 2 wide in each split dimension.  Neighbours may stall this rank
+ * (it waits for them); all ranks must run the same number of steps.
+ * Errors: OEC_ERR_ARG (bad grid/rank, NULL), OEC_ERR_SHAPE (coverage), OEC_ERR_DTYPE,
+ * OEC_ERR_LAYOUT (not TMA-describable), OEC_ERR_ALIAS, OEC_ERR_CUDA. */
+typedef struct oec_hdiff_pipeline oec_hdiff_pipeline; /* opaque */
+
+oec_status oec_hdiff_pipeline_create(const int64_t global_domain[3], int32_t px, int32_t py, int32_t rank,
+                                     const oec_field *coeff, const oec_field *x0, const oec_field *x1,
+                                     oec_hdiff_pipeline **out);
+
+/* This rank's signal pad (library-owned device memory the neighbours write into; 128 bytes):
+ * export it to the other processes with oec_ipc_export. */
+oec_status oec_hdiff_pipeline_signal_pad(const oec_hdiff_pipeline *p, void **pad, int64_t *bytes);
+
+/* Register neighbour `peer_rank` (one of the up to 8 ranks adjacent to this one, corners
+ * included): its x0/x1 descriptors in ITS local coordinates with `data` valid on this device,
+ * and its signal pad.  OEC_ERR_ARG if peer_rank is not adjacent. */
+oec_status oec_hdiff_pipeline_set_peer(oec_hdiff_pipeline *p, int32_t peer_rank, const oec_field *peer_x0,
+                                       const oec_field *peer_x1, void *peer_signal_pad);
+
+/* Enqueue nsteps steps (nsteps kernels) on `stream`; all adjacent ranks must have been
+ * registered.  Asynchronous. */
+oec_status oec_hdiff_pipeline_run(oec_hdiff_pipeline *p, int32_t nsteps, void *stream);
+
+/* Steps completed so far (synchronous read of the device counter; x_t is in x0 iff t is even). */
+oec_status oec_hdiff_pipeline_steps(const oec_hdiff_pipeline *p, int64_t *steps);
+
+oec_status oec_hdiff_pipeline_destroy(oec_hdiff_pipeline *p);
+
+/* CUDA IPC for peer memory between the processes of one node (one process per GPU):
+ * oec_ipc_export writes a 64-byte handle of the cudaMalloc allocation containing dev_ptr plus the
+ * byte offset of dev_ptr in it; oec_ipc_import maps it in this process (peer access over NVLink
+ * enabled) and returns the pointer; oec_ipc_close unmaps it.  Handles of one process cannot be
+ * imported by the same process (use the pointer directly). */
+#define OEC_IPC_HANDLE_BYTES 64
+oec_status oec_ipc_export(const void *dev_ptr, void *handle, int64_t *offset);
+oec_status oec_ipc_import(const void *handle, int64_t offset, void **dev_ptr);
+oec_status oec_ipc_close(void *dev_ptr);
+
+/* ----------------------------------------------------------------------------------------- */
 /* Self-test (used by the GPU test suite).                                                    */
 /* ----------------------------------------------------------------------------------------- */
 /* The vadv kernel computes the fp64 reciprocal with the branch-free instruction sequence of the

@@ -91,9 +91,7 @@ template cudaError_t launch_unpack<float>(const float *, const Box &, const FOf 
 template cudaError_t launch_box_copy<double>(const FV &, const FO &, const Box &, cudaStream_t, int *);
 template cudaError_t launch_box_copy<float>(const FVf &, const FOf &, const Box &, cudaStream_t, int *);
 
-namespace {
-
-int64_t block_start(int64_t n, int p, int r) { return r * (n / p) + std::min<int64_t>(r, n % p); }
+static int64_t block_start(int64_t n, int p, int r) { return r * (n / p) + std::min<int64_t>(r, n % p); }
 
 void subdomain(const int64_t g[3], int px, int py, int rank, int64_t lo[3], int64_t hi[3]) {
     const int ri = rank % px, rj = rank / px;
@@ -104,6 +102,8 @@ void subdomain(const int64_t g[3], int px, int py, int rank, int64_t lo[3], int6
     lo[2] = 0;
     hi[2] = g[2];
 }
+
+namespace {
 
 // messages of `rank` in execution order (see oec.h oec_decomp_plan)
 std::vector<oec_halo_msg> make_plan(const int64_t g[3], int px, int py, int rank, const int32_t wlo[3],

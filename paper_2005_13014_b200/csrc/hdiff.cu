@@ -606,6 +606,225 @@ cudaError_t launch_tma(const TMap &tin, const TMap &tcf, const FOT<T> &out, cons
     return e != cudaSuccess ? e : cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------------------------
+// multi-step hdiff with the halo exchange fused in (north_star (3))
+// ---------------------------------------------------------------------------------------------
+// One launch = one time step t of x_{t+1} = hdiff(x_t) on this rank's sub-domain, x_t in buffer
+// t % 2.  t lives in the signal pad (device memory), so a captured CUDA graph of N launches runs N
+// steps.  Work items are ordered interior first: an interior tile's 13-point diamond never leaves
+// our sub-domain (or reaches only the caller's global outer halo), so it streams through the TMA
+// ring exactly as hdiff_tma and needs nothing from the neighbours.  Boundary tiles come last: the
+// warp waits (once) until every neighbour has completed step t-1, then assembles the tile in
+// shared memory with plain loads -- our cells from our field, the neighbours' cells straight from
+// THEIR fields (peer memory over NVLink, or the same device) -- and runs the same tile code.  No
+// halo is copied, no exchange kernel or NCCL call exists, and the transfer overlaps the interior.
+// When all CTAs are done the last one publishes t+1 into each neighbour's signal pad
+// (st.release.sys) and advances our step counter.  Safety: a neighbour's step t+1 overwrites the
+// buffer we read at step t only in its boundary tiles, which wait for our "step t done".
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long *p, unsigned long long v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+    unsigned long long v;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
+    return v;
+}
+#ifndef PIPE_WAIT_NS
+#define PIPE_WAIT_NS 20000000000ull
+#endif
+
+template <class T>
+__device__ __forceinline__ T pipe_cell(const PipeArgs<T> &a, int b, int i, int j, int k) {
+    // value of x_t at (i, j, k), local coordinates, whoever owns it; cells beyond the 2-wide halo
+    // are never used by the tile arithmetic (0)
+    const int ni = a.d.hi[0], nj = a.d.hi[1];
+    if (i < -2 || i >= ni + 2 || j < -2 || j >= nj + 2) return T(0);
+    const int si = i < 0 ? 0 : (i >= ni ? 2 : 1), sj = j < 0 ? 0 : (j >= nj ? 2 : 1);
+    const int dir = si * 3 + sj;
+    if (dir != 4 && a.nb[dir].exists) {
+        const PeerNb<T> &n = a.nb[dir];
+        return __ldcg(n.x[b] + ((i - n.oi) + (j - n.oj) * n.sj + k * n.sk));  // peer: bypass L1
+    }
+    if (i < a.alo[0] || i >= a.ahi[0] || j < a.alo[1] || j >= a.ahi[1]) return T(0);
+    return a.x[b].p[i + j * a.x[b].sj + k * a.x[b].sk];
+}
+
+template <class T, int V, int JB, int S, int NW>
+__global__ void __launch_bounds__(NW * 32, 1) hdiff_pipe(const __grid_constant__ TMap m0, const __grid_constant__ TMap m1,
+                                                      const __grid_constant__ TMap m_cf,
+                                                      const __grid_constant__ PipeArgs<T> a) {
+    using C = TmaCfg<T, V, JB, S, NW>;
+    constexpr int W = C::W;
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    unsigned char *wbase = smem + warp * S * C::SLOT;
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + NW * S * C::SLOT) + warp * S;
+    const int gw = blockIdx.x * NW + warp, nwt = gridDim.x * NW;
+    const unsigned long long t = *reinterpret_cast<volatile const unsigned long long *>(a.pad + PIPE_PAD_STEP);
+    const int b = (int)(t & 1);
+    const TMap &m_in = b ? m1 : m0;
+    const FOT<T> out = a.y[b ^ 1];
+    const int nk = a.d.hi[2];
+
+    auto in_s = [&](int s) { return reinterpret_cast<T *>(wbase + s * C::SLOT); };
+    auto cf_s = [&](int s) { return reinterpret_cast<T *>(wbase + s * C::SLOT + C::IN_PAD); };
+    const int ns_int = a.sb - a.sa, nc_int = a.cb - a.ca;
+    auto decode_int = [&](int item, int &ib, int &j0, int &k) {
+        ib = (a.sa + item % ns_int) * W;
+        j0 = (a.ca + (item / ns_int) % nc_int) * JB;
+        k = item / (ns_int * nc_int);
+    };
+    auto issue = [&](int item, int s) {
+        int ib, j0, k;
+        decode_int(item, ib, j0, k);
+        mbar_expect_tx(&bars[s], C::IN_BYTES + C::CF_BYTES);
+        tma_load_ijk(in_s(s), m_in, &bars[s], ib - C::LP, j0 - 2, k);
+        tma_load_ijk(cf_s(s), m_cf, &bars[s], ib, j0, k);
+    };
+
+    if (lane == 0) {
+        prefetch_tmap(&m_in.map);
+        prefetch_tmap(&m_cf.map);
+#pragma unroll
+        for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
+        fence_mbar_init();
+    }
+    // ---- interior tiles: the TMA ring of hdiff_tma
+    const int n_int = a.n_int;
+    if (lane == 0) {
+#pragma unroll
+        for (int s = 0; s < S; ++s)
+            if (gw + s * nwt < n_int) issue(gw + s * nwt, s);
+    }
+    __syncwarp();
+    int n = 0;
+    for (int item = gw; item < n_int; item += nwt, ++n) {
+        const int s = n % S;
+        int ib, j0, k;
+        decode_int(item, ib, j0, k);
+        const int nrows = min(JB, a.d.hi[1] - j0);
+        const int i_own = ib + lane * V;
+        T *out_k = out.p + k * out.sk;
+        mbar_wait(&bars[s], (n / S) & 1);
+        if (nrows == JB)
+            hdiff_tile<T, V, JB, C::LP, true>(in_s(s), cf_s(s), out_k, out.sj, j0, JB, i_own, a.d.hi[0], lane);
+        else
+            hdiff_tile<T, V, JB, C::LP, false>(in_s(s), cf_s(s), out_k, out.sj, j0, nrows, i_own, a.d.hi[0], lane);
+        __syncwarp();
+        if (lane == 0) {
+            const int nxt = item + S * nwt;
+            if (nxt < n_int) {
+                fence_proxy_async();
+                issue(nxt, s);
+            }
+        }
+    }
+    // ---- boundary tiles: neighbours' cells read from their memory once they finished step t-1
+    const int per_plane = a.nseg * a.nchunk - ns_int * nc_int;
+    const int nb_items = a.n_items - n_int;
+    bool ready = false;
+    fence_proxy_async();  // slot 0 was last written by TMA (async proxy); now generic stores
+    T *tin = in_s(0), *tcf = cf_s(0);
+    for (int item = gw; item < nb_items; item += nwt) {
+        if (!ready) {
+            if (lane == 0) {
+                // a neighbour that never runs step t-1 (a caller bug) must not hang the GPU:
+                // give up after PIPE_WAIT_NS with a device trap (the launch reports an error)
+                const unsigned long long t0 = globaltimer_ns();
+                for (int dd = 0; dd < 9; ++dd)
+                    if (a.nb[dd].exists)
+                        while (ld_acquire_sys(a.pad + dd) < t) {
+                            __nanosleep(64);
+                            if (globaltimer_ns() - t0 > PIPE_WAIT_NS) __trap();
+                        }
+            }
+            __syncwarp();
+            ready = true;
+        }
+        // boundary item -> (seg, chunk, k): per k-plane, chunk rows below the interior band (all
+        // segments), the band (segments outside [sa, sb)), the rows above (all segments)
+        const int k = item / per_plane;
+        int r = item % per_plane, seg, chunk;
+        const int mid = a.nseg - ns_int;
+        if (r < a.ca * a.nseg) {
+            chunk = r / a.nseg;
+            seg = r % a.nseg;
+        } else if ((r -= a.ca * a.nseg) < nc_int * mid) {
+            chunk = a.ca + r / mid;
+            const int q = r % mid;
+            seg = q < a.sa ? q : a.sb + (q - a.sa);
+        } else {
+            r -= nc_int * mid;
+            chunk = a.cb + r / a.nseg;
+            seg = r % a.nseg;
+        }
+        const int ib = seg * W, j0 = chunk * JB;
+        for (int e = lane; e < (JB + 4) * C::RW; e += 32) {
+            const int rr = e / C::RW, y = e % C::RW;
+            tin[e] = pipe_cell(a, b, ib - C::LP + y, j0 - 2 + rr, k);
+        }
+        for (int e = lane; e < JB * W; e += 32) {
+            const int rr = e / W, x = e % W;
+            const int i = ib + x, j = j0 + rr;
+            tcf[e] = (i < a.d.hi[0] && j < a.d.hi[1]) ? a.cf.p[i + j * a.cf.sj + k * a.cf.sk] : T(0);
+        }
+        __syncwarp();
+        const int nrows = min(JB, a.d.hi[1] - j0);
+        T *out_k = out.p + k * out.sk;
+        if (nrows == JB)
+            hdiff_tile<T, V, JB, C::LP, true>(tin, tcf, out_k, out.sj, j0, JB, ib + lane * V, a.d.hi[0], lane);
+        else
+            hdiff_tile<T, V, JB, C::LP, false>(tin, tcf, out_k, out.sj, j0, nrows, ib + lane * V, a.d.hi[0], lane);
+        __syncwarp();
+    }
+    (void)nk;
+    // ---- publish "step t done" (our outputs written, our reads of the neighbours' x_t finished)
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned long long old = atomicAdd(a.pad + PIPE_PAD_FINISHED, 1ull);
+        if (old == gridDim.x - 1) {
+            a.pad[PIPE_PAD_FINISHED] = 0;
+            __threadfence_system();
+            for (int dd = 0; dd < 9; ++dd)
+                if (a.nb[dd].exists) st_release_sys(a.nb[dd].flag, t + 1);
+            *reinterpret_cast<volatile unsigned long long *>(a.pad + PIPE_PAD_STEP) = t + 1;
+        }
+    }
+}
+
+template <class T, int V, int JB, int S, int NW>
+cudaError_t launch_pipe(const TMap &m0, const TMap &m1, const TMap &mcf, const PipeArgs<T> &a, int nsteps, cudaStream_t st,
+                        int *launches) {
+    using C = TmaCfg<T, V, JB, S, NW>;
+    static bool configured = false;
+    static int blocks_per_sm = 1, sms = 148;
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(hdiff_pipe<T, V, JB, S, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+        if (e != cudaSuccess) return e;
+        int dev;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, hdiff_pipe<T, V, JB, S, NW>, NW * 32, C::SMEM);
+        if (blocks_per_sm < 1) blocks_per_sm = 1;
+        configured = true;
+    }
+    const long long blocks = std::max(1ll, std::min<long long>((a.n_items + NW - 1) / NW, (long long)sms * blocks_per_sm));
+    for (int s = 0; s < nsteps; ++s) {
+        hdiff_pipe<T, V, JB, S, NW><<<(unsigned)blocks, NW * 32, C::SMEM, st>>>(m0, m1, mcf, a);
+        ++*launches;
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+}
+
 template <class T, int V, int JB, int P>
 cudaError_t launch_roll(const FVT<T> &in, const FVT<T> &coeff, const FOT<T> &out, const Dom &d, cudaStream_t s, int *launches) {
     constexpr int W = 32 * V;
@@ -677,6 +896,29 @@ cudaError_t launch_hdiff(const FVT<T> &in, const FVT<T> &coeff, const FOT<T> &ou
     return launch_roll<T, 1, 16, 4>(in, coeff, out, d, s, launches);
 }
 
+template <class T>
+void hdiff_pipe_boxes(const Dom &d, int box_in[3], int box_cf[3], int *tile_w, int *tile_jb) {
+    using C = HdCfg<T>;
+    const bool L = hdiff_large(d);
+    hdiff_tma_boxes<T>(d, box_in, box_cf);
+    *tile_w = 32 * (L ? C::LV : C::V);
+    *tile_jb = L ? C::LJB : C::JB;
+}
+
+template <class T>
+cudaError_t launch_hdiff_pipe(const TMap &m0, const TMap &m1, const TMap &mcf, PipeArgs<T> &a, int nsteps,
+                              cudaStream_t s, int *launches) {
+    using C = HdCfg<T>;
+    if (hdiff_large(a.d)) return launch_pipe<T, C::LV, C::LJB, C::LS, C::LNW>(m0, m1, mcf, a, nsteps, s, launches);
+    return launch_pipe<T, C::V, C::JB, C::S, C::NW>(m0, m1, mcf, a, nsteps, s, launches);
+}
+
+template void hdiff_pipe_boxes<double>(const Dom &, int *, int *, int *, int *);
+template void hdiff_pipe_boxes<float>(const Dom &, int *, int *, int *, int *);
+template cudaError_t launch_hdiff_pipe<double>(const TMap &, const TMap &, const TMap &, PipeArgs<double> &, int,
+                                               cudaStream_t, int *);
+template cudaError_t launch_hdiff_pipe<float>(const TMap &, const TMap &, const TMap &, PipeArgs<float> &, int,
+                                              cudaStream_t, int *);
 template void hdiff_tma_boxes<double>(const Dom &, int *, int *);
 template void hdiff_tma_boxes<float>(const Dom &, int *, int *);
 template cudaError_t launch_hdiff<double>(const FV &, const FV &, const FO &, const Dom &, int, bool, const TMap *,

@@ -78,6 +78,50 @@ cudaError_t launch_unpack(const T *buf, const Box &b, const FOT<T> &dst, cudaStr
 template <class T>
 cudaError_t launch_box_copy(const FVT<T> &src, const FOT<T> &dst, const Box &b, cudaStream_t s, int *launches);
 
+// ---- multi-step hdiff with the halo exchange fused into the kernel:
+// boundary tiles read the neighbours' interior rows straight from their memory (NVLink peer
+// pointers, or plain pointers when the sub-domains share a device); csrc/pipeline.cpp.
+// Directions: index si*3 + sj with si, sj in {0: low side, 1: inside, 2: high side}; 4 = self.
+template <class T>
+struct PeerNb {
+    const T *x[2];             // the neighbour's x0 / x1, origin pointers (its local (0,0,0))
+    int32_t sj, sk;            // its strides (x0 and x1 alike)
+    int32_t oi, oj;            // its local origin in OUR local coordinates
+    unsigned long long *flag;  // the slot of the neighbour's signal pad we write when a step is done
+    int32_t exists, pad_;
+};
+// signal pad words (device memory of the rank that owns the pipeline)
+enum { PIPE_PAD_STEP = 9, PIPE_PAD_FINISHED = 10, PIPE_PAD_WORDS = 16 };
+template <class T>
+struct PipeArgs {
+    PeerNb<T> nb[9];
+    FVT<T> x[2];
+    FOT<T> y[2];       // the same memory as x[0], x[1], writable
+    FVT<T> cf;
+    int32_t alo[2], ahi[2];     // allocated i, j range of x0/x1 (local coordinates)
+    unsigned long long *pad;    // our signal pad: [d] = steps completed by the neighbour in direction d
+    Dom d;                      // [0, N) local domain
+    int32_t nseg, nchunk;       // tiles per k-plane
+    int32_t sa, sb, ca, cb;     // interior tiles (their halo never leaves our sub-domain or the global halo)
+    int32_t n_int, n_items;
+};
+template <class T>
+cudaError_t launch_hdiff_pipe(const TMap &m0, const TMap &m1, const TMap &mcf, PipeArgs<T> &a, int nsteps,
+                              cudaStream_t s, int *launches);
+// TMA boxes of the pipeline kernel (same tile configuration rule as hdiff)
+template <class T>
+void hdiff_pipe_boxes(const Dom &d, int box_in[3], int box_cf[3], int *tile_w, int *tile_jb);
+
+// oec_decomp_create's block split: rank's sub-domain [lo, hi) of global domain g (csrc/halo.cu)
+void subdomain(const int64_t g[3], int px, int py, int rank, int64_t lo[3], int64_t hi[3]);
+
+// field validation shared with runtime.cpp: kernel views (int32 offsets checked), dtype/device
+// agreement (device/dtype start at -2/-1), byte-range overlap
+template <class V>
+oec_status field_view(const oec_field *f, const char *what, V *v);
+oec_status field_check(const oec_field *f, const char *what, int *device, int *dtype);
+bool field_overlap(const oec_field *a, const oec_field *b);
+
 // error plumbing; launch count reported by oec_last_launch_count
 oec_status set_error(oec_status st, const char *fmt, ...);
 void set_launch_count(int n);

@@ -221,6 +221,24 @@ static oec_status make_view(const oec_field *f, const char *what, V *v) {
     return OEC_OK;
 }
 
+// exported to the other translation units (csrc/pipeline.cpp)
+template <class V>
+oec_status field_view(const oec_field *f, const char *what, V *v) {
+    return make_view(f, what, v);
+}
+template oec_status field_view<FVT<double>>(const oec_field *, const char *, FVT<double> *);
+template oec_status field_view<FVT<float>>(const oec_field *, const char *, FVT<float> *);
+template oec_status field_view<FOT<double>>(const oec_field *, const char *, FOT<double> *);
+template oec_status field_view<FOT<float>>(const oec_field *, const char *, FOT<float> *);
+oec_status field_check(const oec_field *f, const char *what, int *device, int *dtype) {
+    return check_field(f, what, device, dtype);
+}
+bool field_overlap(const oec_field *a, const oec_field *b) {
+    uintptr_t alo, ahi, blo, bhi;
+    if (!span_bytes(a, &alo, &ahi) || !span_bytes(b, &blo, &bhi)) return false;
+    return alo < bhi && blo < ahi;
+}
+
 static oec_status check_domain(const int64_t *lo, const int64_t *hi) {
     if (!lo || !hi) return set_error(OEC_ERR_ARG, "NULL domain");
     for (int d = 0; d < 3; ++d) {

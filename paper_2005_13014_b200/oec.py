@@ -96,6 +96,16 @@ SIGNATURES = {
     "oec_halo_exchange_local": (C.c_int, [C.POINTER(C.c_int64), C.c_int32, C.c_int32, _PP, C.c_int32,
                                           C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.c_void_p]),
     "oec_decomp_destroy": (C.c_int, [C.c_void_p]),
+    "oec_hdiff_pipeline_create": (C.c_int, [C.POINTER(C.c_int64), C.c_int32, C.c_int32, C.c_int32, _P, _P, _P,
+                                            C.POINTER(C.c_void_p)]),
+    "oec_hdiff_pipeline_signal_pad": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_int64)]),
+    "oec_hdiff_pipeline_set_peer": (C.c_int, [C.c_void_p, C.c_int32, _P, _P, C.c_void_p]),
+    "oec_hdiff_pipeline_run": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p]),
+    "oec_hdiff_pipeline_steps": (C.c_int, [C.c_void_p, C.POINTER(C.c_int64)]),
+    "oec_hdiff_pipeline_destroy": (C.c_int, [C.c_void_p]),
+    "oec_ipc_export": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(C.c_int64)]),
+    "oec_ipc_import": (C.c_int, [C.c_void_p, C.c_int64, C.POINTER(C.c_void_p)]),
+    "oec_ipc_close": (C.c_int, [C.c_void_p]),
     "oec_selftest_rcp": (C.c_int, [C.c_ulonglong, C.c_ulonglong, C.POINTER(C.c_ulonglong), C.POINTER(C.c_ulonglong)]),
 }
 
@@ -424,3 +434,77 @@ def oec_selftest_rcp(n: int, seed: int = 1):
     bad, used = C.c_ulonglong(), C.c_ulonglong()
     _check(lib().oec_selftest_rcp(n, seed, C.byref(bad), C.byref(used)))
     return bad.value, used.value
+
+
+# ---------------------------------------------------------------------------------------------
+# multi-step hdiff with the halo exchange fused into the kernel (oec_hdiff_pipeline)
+# ---------------------------------------------------------------------------------------------
+OEC_IPC_HANDLE_BYTES = 64
+
+
+class HdiffPipeline:
+    """oec_hdiff_pipeline: x_{t+1} = hdiff(x_t) on one rank's sub-domain, neighbours' cells read
+    from their memory inside the kernel.  Keeps the Field objects alive."""
+
+    def __init__(self, global_domain, px: int, py: int, rank: int, coeff: Field, x0: Field, x1: Field):
+        h = C.c_void_p()
+        _check(lib().oec_hdiff_pipeline_create(_i64(global_domain), px, py, rank, coeff.ptr, x0.ptr, x1.ptr, C.byref(h)))
+        self.handle = h
+        self._keep = [coeff, x0, x1]
+
+    def signal_pad(self) -> Tuple[int, int]:
+        p, n = C.c_void_p(), C.c_int64()
+        _check(lib().oec_hdiff_pipeline_signal_pad(self.handle, C.byref(p), C.byref(n)))
+        return p.value, n.value
+
+    def set_peer(self, peer_rank: int, peer_x0: Field, peer_x1: Field, peer_pad: int):
+        _check(lib().oec_hdiff_pipeline_set_peer(self.handle, peer_rank, peer_x0.ptr, peer_x1.ptr, C.c_void_p(peer_pad)))
+        self._keep += [peer_x0, peer_x1]
+
+    def run(self, nsteps: int, stream=None):
+        _check(lib().oec_hdiff_pipeline_run(self.handle, nsteps, _stream(stream)))
+
+    def steps(self) -> int:
+        v = C.c_int64()
+        _check(lib().oec_hdiff_pipeline_steps(self.handle, C.byref(v)))
+        return v.value
+
+    def __del__(self):
+        try:
+            if self.handle:
+                lib().oec_hdiff_pipeline_destroy(self.handle)
+                self.handle = None
+        except Exception:
+            pass
+
+
+def oec_ipc_export(dev_ptr: int) -> Tuple[bytes, int]:
+    h = (C.c_ubyte * OEC_IPC_HANDLE_BYTES)()
+    off = C.c_int64()
+    _check(lib().oec_ipc_export(C.c_void_p(dev_ptr), h, C.byref(off)))
+    return bytes(h), off.value
+
+
+def oec_ipc_import(handle: bytes, offset: int) -> int:
+    h = (C.c_ubyte * OEC_IPC_HANDLE_BYTES).from_buffer_copy(handle)
+    p = C.c_void_p()
+    _check(lib().oec_ipc_import(h, int(offset), C.byref(p)))
+    return p.value
+
+
+def oec_ipc_close(dev_ptr: int):
+    _check(lib().oec_ipc_close(C.c_void_p(dev_ptr)))
+
+
+def field_descriptor(f: Field) -> dict:
+    """Plain-data description of a field (to send to another process with its IPC handle)."""
+    d = f.desc
+    return dict(lb=tuple(d.lb), ub=tuple(d.ub), stride=tuple(d.stride), dtype=d.dtype, device=d.device)
+
+
+def field_at(ptr: int, desc: dict, device: int) -> Field:
+    """A borrowed field over `ptr` (e.g. an IPC-imported peer allocation) with a peer's layout."""
+    d = OecField()
+    _check(lib().oec_field_wrap(C.c_void_p(ptr), _i64(desc["lb"]), _i64(desc["ub"]), _i64(desc["stride"]),
+                                desc["dtype"], device, C.byref(d)))
+    return Field(d)
