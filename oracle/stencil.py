@@ -134,8 +134,17 @@ def run_unfused(prog: Program, fields: Dict[str, HostField], scalars: Dict[str, 
     scalars = {k: dt.type(v) for k, v in scalars.items()}
     env: Dict[str, HostField] = {n: fields[n] for n in prog.inputs}
     # universe: the bounding box of all input allocations (k-invariant fields: all k)
-    ulo = [min(f.lb[d] for f in env.values() if not (d == 2 and f.k_invariant)) for d in range(3)]
-    uhi = [max(f.ub[d] for f in env.values() if not (d == 2 and f.k_invariant)) for d in range(3)]
+    # universe: the bounding box of the domain and all input allocations (k-invariant fields: no
+    # k range), grown by the longest chain of access offsets -- a temporary may be needed (and be
+    # computable) beyond the inputs' box when a consumer reads it at an offset.  It
+    # only bounds applies whose accesses leave a dimension unconstrained (constants, k-invariant
+    # inputs); every other box is the intersection of its accesses' in-range boxes.
+    margin = [sum(max([abs(acc[1 + d]) for acc in accesses(ap, prog.scalars)] + [0]) for ap in prog.applies)
+              for d in range(3)]
+    ulo = [min([domain_lo[d]] + [f.lb[d] for f in env.values() if not (d == 2 and f.k_invariant)]) - margin[d]
+           for d in range(3)]
+    uhi = [max([domain_hi[d]] + [f.ub[d] for f in env.values() if not (d == 2 and f.k_invariant)]) + margin[d]
+           for d in range(3)]
     for ap in prog.applies:
         lo, hi = list(ulo), list(uhi)
         for name, di, dj, dk in accesses(ap, prog.scalars):
