@@ -197,6 +197,77 @@ oec_status oec_apply_program(const char *program, const oec_field *const *inputs
 int32_t oec_last_launch_count(void);
 
 /* ----------------------------------------------------------------------------------------- */
+/* Stencil programs from text: shape inference, inlining, unrolling and size-specialised JIT   */
+/* (§4 the stencil dialect, §5.1 inlining P:431 and unrolling    */
+/* P:447, §5.2 shape inference P:480-482, size specialization P:338).                          */
+/* ----------------------------------------------------------------------------------------- */
+/* The stencil language mirrors the dialect's program structure:
+ *
+ *   program NAME                       # a stencil program
+ *   input  NAME [: ij | : ijk]         # stencil.load of an input array; ij = k-invariant (2D)
+ *   scalar NAME [= NUMBER]             # a scalar parameter (default value)
+ *   output NAME                        # an output array
+ *   apply  R1[, R2 ...] {              # stencil.apply defining results R1, R2, ...
+ *       LOCAL = EXPR                   #   scalar values inside the operator (SSA)
+ *       return EXPR[, EXPR ...]        #   stencil.return, one value per result
+ *   }
+ *   apply  R = EXPR                    # short form of a one-result operator
+ *   store  R -> OUTPUT                 # stencil.store of a result over the domain
+ *   end                                # optional
+ *
+ *   EXPR: NUMBER | SCALAR | LOCAL | NAME | NAME[di, dj, dk] (stencil.access of an input or an
+ *   EARLIER result at a constant offset; NAME alone = [0, 0, 0]) | - EXPR | EXPR (+ - * /)
+ *   EXPR | select(COND, EXPR, EXPR) (loop.if / select) | min(a, b) := b < a ? b : a |
+ *   max(a, b) := b > a ? b : a | abs(EXPR) | sqrt(EXPR) | ( EXPR ).
+ *   COND: EXPR (< > <= >= == !=) EXPR | COND && COND | COND || COND | ! COND | ( COND ).
+ *   Precedence (low -> high): ||, &&, comparisons, + -, * /, unary; binary operators associate
+ *   to the left, so `a + b + c` is `(a + b) + c`: the evaluation order of every program is fixed
+ *   by its text, and results are bit-identical to any evaluator that follows it.  `#` starts a
+ *   comment; `;` and newlines are whitespace.
+ * Semantics: IEEE arithmetic in the fields' precision (f64, or binary32 with every literal and
+ * scalar rounded once), no contraction, correctly rounded / and sqrt.  An operator reads inputs
+ * and EARLIER results only (the def-use graph is acyclic); outputs are never read and
+ * inputs never stored.  Operators no output depends on are dead.
+ * Shape inference gives each input its access extent (oec_program_input): the
+ * union over its readers of their iteration domains grown by the access offsets, where an
+ * operator's iteration domain is the bounding box of what its own readers need and a stored
+ * result is needed on the domain.
+ *
+ * Variants (oec_apply_program): AUTO / NAIVE = inline, one generated kernel, one thread
+ * per point, every operator recomputed at every offset its readers use, each (operator, offset)
+ * and (input, offset) evaluated once per thread (CSE); UNROLL2 / UNROLL4 = inline +
+ * unroll along j; UNFUSED = the original level, one kernel per live operator over
+ * its inferred domain, temporaries in a library device workspace (single stream at a time).
+ * Kernels are generated with the domain size and all strides as constants, compiled by
+ * NVRTC for sm_100a on first use of a (program, dtype, variant, size, strides, device) and
+ * cached for the life of the process; the first call of a specialisation must not be inside a
+ * CUDA graph capture.  NVRTC is loaded at run time (libnvrtc.so.12): OEC_ERR_UNSUPPORTED if
+ * absent. */
+
+/* Parse, verify and shape-infer `source`; register the program under its `program NAME` so that
+ * oec_program_info / _input / _output / _scalar and oec_apply_program accept the name.
+ * *name (may be NULL): the registered name, valid until oec_program_destroy.  Errors:
+ * OEC_ERR_ARG with "line L:C: message" for syntax / type / definition errors, a name that is a
+ * builtin program or already registered. */
+oec_status oec_program_create(const char *source, const char **name);
+
+/* Unregister a program created by oec_program_create (its cached kernels stay loaded; launches
+ * already enqueued are unaffected).  OEC_ERR_ARG for builtins and unknown names. */
+oec_status oec_program_destroy(const char *program);
+
+/* The CUDA source oec_apply_program would compile for these fields / domain / variant (no launch,
+ * no device memory touched: descriptors may hold any pointers of any device value).  source may
+ * be NULL; at most capacity-1 bytes are written plus a NUL; *length = the full source length.
+ * compile != 0: also compile it with NVRTC for sm_100a (host only, no GPU needed) and report the
+ * cubin size in *cubin_bytes (0 otherwise).  Errors: OEC_ERR_ARG (not a registered text
+ * program, counts, variant), field errors as oec_apply_program, OEC_ERR_CUDA with the NVRTC log
+ * on a compile error, OEC_ERR_UNSUPPORTED without NVRTC. */
+oec_status oec_program_generate(const char *program, const oec_field *const *inputs, int32_t n_inputs,
+                                oec_field *const *outputs, int32_t n_outputs, const int64_t dom_lb[3],
+                                const int64_t dom_ub[3], int32_t variant, int32_t compile, char *source,
+                                int64_t capacity, int64_t *length, int64_t *cubin_bytes);
+
+/* ----------------------------------------------------------------------------------------- */
 /* Horizontal domain decomposition + halo exchange (a8; north_star (3)).  Not in PAPER.md. */
 /* ----------------------------------------------------------------------------------------- */
 typedef struct oec_decomp oec_decomp; /* opaque */

@@ -3,6 +3,12 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <array>
+#include <functional>
+#include <memory>
+#include <string>
+#include <vector>
+
 #include "../../include/oec.h"
 #include "tma.h"
 
@@ -125,6 +131,27 @@ bool field_overlap(const oec_field *a, const oec_field *b);
 // error plumbing; launch count reported by oec_last_launch_count
 oec_status set_error(oec_status st, const char *fmt, ...);
 void set_launch_count(int n);
+
+// A program as the validation / host-staging layer (runtime.cpp apply) sees it: a builtin
+// registry entry or a program compiled from stencil-language text (csrc/jit.cpp).  Extents are
+// the shape-inference result relative to the domain.
+struct ProgDesc {
+    std::string name;
+    std::vector<std::string> in_names, out_names, sc_names;
+    std::vector<std::array<int, 3>> in_lo, in_hi;
+    std::vector<int> in_kinv;
+    std::vector<double> sc_dflt;
+    int min_k = 1;          // smallest K the program accepts (vadv: 2)
+    bool unroll_ok = true;  // OEC_VARIANT_UNROLL2/4 meaningful
+    // device runner: called with validated device fields (registry order) and complete scalars
+    std::function<oec_status(int dtype, const oec_field *const *in, oec_field *const *out, const double *sc,
+                             const int64_t *lo, const int64_t *hi, int variant, cudaStream_t s)>
+        run;
+};
+// JIT registry (csrc/jit.cpp): the program registered under `name`, or null
+std::shared_ptr<const ProgDesc> jit_lookup(const char *name);
+// true for the hand-written programs of the builtin registry (runtime.cpp)
+bool builtin_program(const char *name);
 
 }  // namespace oec
 

@@ -10,6 +10,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <memory>
 #include <mutex>
 #include <vector>
 
@@ -397,77 +398,123 @@ static oec_status run_device(int p, const oec_field *const *in, oec_field *const
     return OEC_OK;
 }
 
-static oec_status apply(int p, const oec_field *const *in, int n_in, oec_field *const *out, int n_out,
+// builtin registry entries as generic descriptors (built once)
+static const ProgDesc &builtin_desc(int p) {
+    static std::vector<ProgDesc> descs;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        descs.resize(OEC_NPROG);
+        for (int q = 0; q < OEC_NPROG; ++q) {
+            const ProgSpec &S = PROGS[q];
+            ProgDesc &D = descs[q];
+            D.name = S.name;
+            for (int r = 0; r < S.n_in; ++r) {
+                D.in_names.push_back(S.in[r].name);
+                D.in_lo.push_back({S.in[r].lo[0], S.in[r].lo[1], S.in[r].lo[2]});
+                D.in_hi.push_back({S.in[r].hi[0], S.in[r].hi[1], S.in[r].hi[2]});
+                D.in_kinv.push_back(S.in[r].k_invariant);
+            }
+            for (int r = 0; r < S.n_out; ++r) D.out_names.push_back(S.out[r]);
+            for (int r = 0; r < S.n_sc; ++r) {
+                D.sc_names.push_back(S.sc[r].name);
+                D.sc_dflt.push_back(S.sc[r].dflt);
+            }
+            D.min_k = q == OEC_PROG_VADV ? 2 : 1;
+            D.unroll_ok = q != OEC_PROG_VADV;
+            D.run = [q](int dtype, const oec_field *const *in, oec_field *const *out, const double *sc, const int64_t *lo,
+                        const int64_t *hi, int variant, cudaStream_t s) {
+                return dtype == OEC_F32 ? run_device<float>(q, in, out, sc, lo, hi, variant, s)
+                                        : run_device<double>(q, in, out, sc, lo, hi, variant, s);
+            };
+        }
+    });
+    return descs[p];
+}
+
+// the program named `name`: a builtin, else a program registered with oec_program_create
+static std::shared_ptr<const ProgDesc> lookup(const char *name) {
+    int p = find_prog(name);
+    if (p >= 0) return std::shared_ptr<const ProgDesc>(&builtin_desc(p), [](const ProgDesc *) {});
+    return name ? jit_lookup(name) : nullptr;
+}
+
+bool builtin_program(const char *name) { return find_prog(name) >= 0; }
+
+static oec_status apply(const ProgDesc &P, const oec_field *const *in, int n_in, oec_field *const *out, int n_out,
                         const double *scalars, int n_sc, const int64_t *lo, const int64_t *hi, int variant,
                         void *stream) {
-    const ProgSpec &P = PROGS[p];
+    const char *pname = P.name.c_str();
+    const int P_n_in = (int)P.in_names.size(), P_n_out = (int)P.out_names.size(), P_n_sc = (int)P.sc_names.size();
     g_err[0] = 0;
     g_launches = 0;
-    if (n_in != P.n_in || n_out != P.n_out)
-        return set_error(OEC_ERR_ARG, "%s: expects %d inputs / %d outputs, got %d / %d", P.name, P.n_in, P.n_out, n_in, n_out);
-    if (!in || !out) return set_error(OEC_ERR_ARG, "%s: NULL input/output array", P.name);
-    if (n_sc != 0 && n_sc != P.n_sc) return set_error(OEC_ERR_ARG, "%s: expects %d scalars, got %d", P.name, P.n_sc, n_sc);
-    if (n_sc && !scalars) return set_error(OEC_ERR_ARG, "%s: NULL scalars", P.name);
+    if (n_in != P_n_in || n_out != P_n_out)
+        return set_error(OEC_ERR_ARG, "%s: expects %d inputs / %d outputs, got %d / %d", pname, P_n_in, P_n_out, n_in, n_out);
+    if (!in || !out) return set_error(OEC_ERR_ARG, "%s: NULL input/output array", pname);
+    if (n_sc != 0 && n_sc != P_n_sc) return set_error(OEC_ERR_ARG, "%s: expects %d scalars, got %d", pname, P_n_sc, n_sc);
+    if (n_sc && !scalars) return set_error(OEC_ERR_ARG, "%s: NULL scalars", pname);
     if (variant < OEC_VARIANT_AUTO || variant > OEC_VARIANT_UNROLL4)
-        return set_error(OEC_ERR_ARG, "%s: unknown variant %d", P.name, variant);
-    if ((variant == OEC_VARIANT_UNROLL2 || variant == OEC_VARIANT_UNROLL4) && p == OEC_PROG_VADV)
+        return set_error(OEC_ERR_ARG, "%s: unknown variant %d", pname, variant);
+    if ((variant == OEC_VARIANT_UNROLL2 || variant == OEC_VARIANT_UNROLL4) && !P.unroll_ok)
         return set_error(OEC_ERR_UNSUPPORTED,
-                         "vadv: stencil unrolling (P:447) does not apply to the vertical solver (independent columns, "
-                         "no shared producers for CSE to remove)");
+                         "%s: stencil unrolling (P:447) does not apply to the vertical solver (independent columns, "
+                         "no shared producers for CSE to remove)", pname);
     oec_status st = check_domain(lo, hi);
     if (st) return st;
     int device = -2, dtype = -1;
-    for (int q = 0; q < P.n_in; ++q)
-        if ((st = check_field(in[q], P.in[q].name, &device, &dtype))) return st;
-    for (int q = 0; q < P.n_out; ++q)
-        if ((st = check_field(out[q], P.out[q], &device, &dtype))) return st;
-    auto run = dtype == OEC_F32 ? run_device<float> : run_device<double>;
-    for (int q = 0; q < P.n_out; ++q)
+    for (int q = 0; q < P_n_in; ++q)
+        if ((st = check_field(in[q], P.in_names[q].c_str(), &device, &dtype))) return st;
+    for (int q = 0; q < P_n_out; ++q)
+        if ((st = check_field(out[q], P.out_names[q].c_str(), &device, &dtype))) return st;
+    for (int q = 0; q < P_n_out; ++q)
         if (is_k_invariant(out[q]))
-            return set_error(OEC_ERR_SHAPE, "%s: output %s must not be k-invariant", P.name, P.out[q]);
-    if (p == OEC_PROG_VADV && hi[2] - lo[2] < 2)
-        return set_error(OEC_ERR_SHAPE, "vadv: K = %lld < 2 (the k=0 and k=K-1 rows would coincide)", (long long)(hi[2] - lo[2]));
+            return set_error(OEC_ERR_SHAPE, "%s: output %s must not be k-invariant", pname, P.out_names[q].c_str());
+    if (hi[2] - lo[2] < P.min_k)
+        return set_error(OEC_ERR_SHAPE, "%s: K = %lld < %d (the k=0 and k=K-1 rows would coincide)", pname,
+                         (long long)(hi[2] - lo[2]), P.min_k);
     static const int Z[3] = {0, 0, 0};
     bool empty = domain_empty(lo, hi);
     if (!empty) {
-        for (int q = 0; q < P.n_in; ++q)
-            if ((st = check_cover(in[q], P.in[q].name, lo, hi, P.in[q].lo, P.in[q].hi, P.in[q].k_invariant))) return st;
-        for (int q = 0; q < P.n_out; ++q)
-            if ((st = check_cover(out[q], P.out[q], lo, hi, Z, Z, 0))) return st;
+        for (int q = 0; q < P_n_in; ++q)
+            if ((st = check_cover(in[q], P.in_names[q].c_str(), lo, hi, P.in_lo[q].data(), P.in_hi[q].data(),
+                                  P.in_kinv[q])))
+                return st;
+        for (int q = 0; q < P_n_out; ++q)
+            if ((st = check_cover(out[q], P.out_names[q].c_str(), lo, hi, Z, Z, 0))) return st;
     }
     // aliasing: an output may not overlap any input or another output
-    for (int q = 0; q < P.n_out; ++q) {
+    for (int q = 0; q < P_n_out; ++q) {
         uintptr_t a0, a1;
         span_bytes(out[q], &a0, &a1);
-        for (int r = 0; r < P.n_in; ++r) {
+        for (int r = 0; r < P_n_in; ++r) {
             uintptr_t b0, b1;
             span_bytes(in[r], &b0, &b1);
             if (a0 < b1 && b0 < a1)
-                return set_error(OEC_ERR_ALIAS, "%s: output %s overlaps input %s (P:381 alias-free parameters)", P.name,
-                                 P.out[q], P.in[r].name);
+                return set_error(OEC_ERR_ALIAS, "%s: output %s overlaps input %s (P:381 alias-free parameters)", pname,
+                                 P.out_names[q].c_str(), P.in_names[r].c_str());
         }
         for (int r = 0; r < q; ++r) {
             uintptr_t b0, b1;
             span_bytes(out[r], &b0, &b1);
             if (a0 < b1 && b0 < a1)
-                return set_error(OEC_ERR_ALIAS, "%s: outputs %s and %s overlap", P.name, P.out[q], P.out[r]);
+                return set_error(OEC_ERR_ALIAS, "%s: outputs %s and %s overlap", pname, P.out_names[q].c_str(),
+                                 P.out_names[r].c_str());
         }
     }
-    double sc[2];
-    for (int q = 0; q < P.n_sc; ++q) sc[q] = n_sc ? scalars[q] : P.sc[q].dflt;
+    std::vector<double> sc(P_n_sc + 1);
+    for (int q = 0; q < P_n_sc; ++q) sc[q] = n_sc ? scalars[q] : P.sc_dflt[q];
     if (empty) return OEC_OK;
     cudaStream_t s = (cudaStream_t)stream;
 
-    if (device >= 0) return run(p, in, out, sc, lo, hi, variant, s);
-    if (device != OEC_DEVICE_HOST) return set_error(OEC_ERR_ARG, "%s: invalid device %d", P.name, device);
+    if (device >= 0) return P.run(dtype, in, out, sc.data(), lo, hi, variant, s);
+    if (device != OEC_DEVICE_HOST) return set_error(OEC_ERR_ARG, "%s: invalid device %d", pname, device);
 
     // ---- end-to-end path: stage host fields through cached device buffers ----
     std::lock_guard<std::mutex> lock(g_stage.mu);
-    oec_field din[9], dout[3];
-    const oec_field *pin[9];
-    oec_field *pout[3];
+    std::vector<oec_field> din(P_n_in), dout(P_n_out);
+    std::vector<const oec_field *> pin(P_n_in);
+    std::vector<oec_field *> pout(P_n_out);
     size_t slot = 0;
-    for (int q = 0; q < P.n_in; ++q) {
+    for (int q = 0; q < P_n_in; ++q) {
         uintptr_t b0, b1;
         span_bytes(in[q], &b0, &b1);
         void *dptr;
@@ -476,10 +523,11 @@ static oec_status apply(int p, const oec_field *const *in, int n_in, oec_field *
         din[q].device = 0;
         din[q].data = (char *)dptr + ((uintptr_t)in[q]->data - b0);
         cudaError_t e = cudaMemcpyAsync(dptr, (const void *)b0, b1 - b0, cudaMemcpyHostToDevice, s);
-        if (e != cudaSuccess) return set_error(OEC_ERR_CUDA, "H2D copy of %s: %s", P.in[q].name, cudaGetErrorString(e));
+        if (e != cudaSuccess)
+            return set_error(OEC_ERR_CUDA, "H2D copy of %s: %s", P.in_names[q].c_str(), cudaGetErrorString(e));
         pin[q] = &din[q];
     }
-    for (int q = 0; q < P.n_out; ++q) {
+    for (int q = 0; q < P_n_out; ++q) {
         uintptr_t b0, b1;
         span_bytes(out[q], &b0, &b1);
         void *dptr;
@@ -489,14 +537,15 @@ static oec_status apply(int p, const oec_field *const *in, int n_in, oec_field *
         dout[q].data = (char *)dptr + ((uintptr_t)out[q]->data - b0);
         pout[q] = &dout[q];
     }
-    if ((st = run(p, pin, pout, sc, lo, hi, variant, s))) return st;
+    if ((st = P.run(dtype, pin.data(), pout.data(), sc.data(), lo, hi, variant, s))) return st;
     int launches = g_launches;
-    for (int q = 0; q < P.n_out; ++q) {
+    for (int q = 0; q < P_n_out; ++q) {
         cudaError_t e = d2h_box(out[q], &dout[q], lo, hi, s);
-        if (e != cudaSuccess) return set_error(OEC_ERR_CUDA, "D2H copy of %s: %s", P.out[q], cudaGetErrorString(e));
+        if (e != cudaSuccess)
+            return set_error(OEC_ERR_CUDA, "D2H copy of %s: %s", P.out_names[q].c_str(), cudaGetErrorString(e));
     }
     cudaError_t e = cudaStreamSynchronize(s);
-    if (e != cudaSuccess) return set_error(OEC_ERR_CUDA, "%s: %s", P.name, cudaGetErrorString(e));
+    if (e != cudaSuccess) return set_error(OEC_ERR_CUDA, "%s: %s", pname, cudaGetErrorString(e));
     g_launches = launches;
     return OEC_OK;
 }
@@ -622,43 +671,47 @@ oec_status oec_field_destroy(oec_field *f) {
 }
 
 oec_status oec_program_info(const char *program, int32_t *n_inputs, int32_t *n_outputs, int32_t *n_scalars) {
-    int p = find_prog(program);
-    if (p < 0) return set_error(OEC_ERR_ARG, "unknown program '%s'", program ? program : "(null)");
-    if (n_inputs) *n_inputs = PROGS[p].n_in;
-    if (n_outputs) *n_outputs = PROGS[p].n_out;
-    if (n_scalars) *n_scalars = PROGS[p].n_sc;
+    g_err[0] = 0;
+    auto P = lookup(program);
+    if (!P) return set_error(OEC_ERR_ARG, "unknown program '%s'", program ? program : "(null)");
+    if (n_inputs) *n_inputs = (int32_t)P->in_names.size();
+    if (n_outputs) *n_outputs = (int32_t)P->out_names.size();
+    if (n_scalars) *n_scalars = (int32_t)P->sc_names.size();
     return OEC_OK;
 }
 
+// names returned by the queries below are valid while the program stays registered (builtins: always)
 oec_status oec_program_input(const char *program, int32_t idx, const char **name, int64_t lo[3], int64_t hi[3],
                              int32_t *k_invariant) {
-    int p = find_prog(program);
-    if (p < 0) return set_error(OEC_ERR_ARG, "unknown program '%s'", program ? program : "(null)");
-    if (idx < 0 || idx >= PROGS[p].n_in) return set_error(OEC_ERR_ARG, "%s: input index %d out of range", program, idx);
-    const InSpec &s = PROGS[p].in[idx];
-    if (name) *name = s.name;
+    g_err[0] = 0;
+    auto P = lookup(program);
+    if (!P) return set_error(OEC_ERR_ARG, "unknown program '%s'", program ? program : "(null)");
+    if (idx < 0 || idx >= (int)P->in_names.size()) return set_error(OEC_ERR_ARG, "%s: input index %d out of range", program, idx);
+    if (name) *name = P->in_names[idx].c_str();
     for (int d = 0; d < 3; ++d) {
-        if (lo) lo[d] = s.lo[d];
-        if (hi) hi[d] = s.hi[d];
+        if (lo) lo[d] = P->in_lo[idx][d];
+        if (hi) hi[d] = P->in_hi[idx][d];
     }
-    if (k_invariant) *k_invariant = s.k_invariant;
+    if (k_invariant) *k_invariant = P->in_kinv[idx];
     return OEC_OK;
 }
 
 oec_status oec_program_output(const char *program, int32_t idx, const char **name) {
-    int p = find_prog(program);
-    if (p < 0) return set_error(OEC_ERR_ARG, "unknown program '%s'", program ? program : "(null)");
-    if (idx < 0 || idx >= PROGS[p].n_out) return set_error(OEC_ERR_ARG, "%s: output index %d out of range", program, idx);
-    if (name) *name = PROGS[p].out[idx];
+    g_err[0] = 0;
+    auto P = lookup(program);
+    if (!P) return set_error(OEC_ERR_ARG, "unknown program '%s'", program ? program : "(null)");
+    if (idx < 0 || idx >= (int)P->out_names.size()) return set_error(OEC_ERR_ARG, "%s: output index %d out of range", program, idx);
+    if (name) *name = P->out_names[idx].c_str();
     return OEC_OK;
 }
 
 oec_status oec_program_scalar(const char *program, int32_t idx, const char **name, double *default_value) {
-    int p = find_prog(program);
-    if (p < 0) return set_error(OEC_ERR_ARG, "unknown program '%s'", program ? program : "(null)");
-    if (idx < 0 || idx >= PROGS[p].n_sc) return set_error(OEC_ERR_ARG, "%s: scalar index %d out of range", program, idx);
-    if (name) *name = PROGS[p].sc[idx].name;
-    if (default_value) *default_value = PROGS[p].sc[idx].dflt;
+    g_err[0] = 0;
+    auto P = lookup(program);
+    if (!P) return set_error(OEC_ERR_ARG, "unknown program '%s'", program ? program : "(null)");
+    if (idx < 0 || idx >= (int)P->sc_names.size()) return set_error(OEC_ERR_ARG, "%s: scalar index %d out of range", program, idx);
+    if (name) *name = P->sc_names[idx].c_str();
+    if (default_value) *default_value = P->sc_dflt[idx];
     return OEC_OK;
 }
 
@@ -666,7 +719,7 @@ oec_status oec_hdiff_variant(const oec_field *in, const oec_field *coeff, oec_fi
                              const int64_t dom_ub[3], int32_t variant, void *stream) {
     const oec_field *ins[2] = {in, coeff};
     oec_field *outs[1] = {out};
-    return apply(OEC_PROG_HDIFF, ins, 2, outs, 1, nullptr, 0, dom_lb, dom_ub, variant, stream);
+    return apply(builtin_desc(OEC_PROG_HDIFF), ins, 2, outs, 1, nullptr, 0, dom_lb, dom_ub, variant, stream);
 }
 
 oec_status oec_hdiff(const oec_field *in, const oec_field *coeff, oec_field *out, const int64_t dom_lb[3],
@@ -679,16 +732,16 @@ oec_status oec_vadv(const oec_field *u_stage, const oec_field *wcon, const oec_f
                     const int64_t dom_lb[3], const int64_t dom_ub[3], void *stream) {
     const oec_field *ins[5] = {u_stage, wcon, u_pos, utens, utens_stage_in};
     oec_field *outs[1] = {utens_stage_out};
-    return apply(OEC_PROG_VADV, ins, 5, outs, 1, &dtr_stage, 1, dom_lb, dom_ub, OEC_VARIANT_AUTO, stream);
+    return apply(builtin_desc(OEC_PROG_VADV), ins, 5, outs, 1, &dtr_stage, 1, dom_lb, dom_ub, OEC_VARIANT_AUTO, stream);
 }
 
 oec_status oec_apply_program(const char *program, const oec_field *const *inputs, int32_t n_inputs,
                              oec_field *const *outputs, int32_t n_outputs, const double *scalars, int32_t n_scalars,
                              const int64_t dom_lb[3], const int64_t dom_ub[3], int32_t variant, void *stream) {
     g_err[0] = 0;
-    int p = find_prog(program);
-    if (p < 0) return set_error(OEC_ERR_ARG, "unknown program '%s'", program ? program : "(null)");
-    return apply(p, inputs, n_inputs, outputs, n_outputs, scalars, n_scalars, dom_lb, dom_ub, variant, stream);
+    auto P = lookup(program);
+    if (!P) return set_error(OEC_ERR_ARG, "unknown program '%s'", program ? program : "(null)");
+    return apply(*P, inputs, n_inputs, outputs, n_outputs, scalars, n_scalars, dom_lb, dom_ub, variant, stream);
 }
 
 }  // extern "C"

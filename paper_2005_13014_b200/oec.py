@@ -106,6 +106,11 @@ SIGNATURES = {
     "oec_ipc_export": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(C.c_int64)]),
     "oec_ipc_import": (C.c_int, [C.c_void_p, C.c_int64, C.POINTER(C.c_void_p)]),
     "oec_ipc_close": (C.c_int, [C.c_void_p]),
+    "oec_program_create": (C.c_int, [C.c_char_p, C.POINTER(C.c_char_p)]),
+    "oec_program_destroy": (C.c_int, [C.c_char_p]),
+    "oec_program_generate": (C.c_int, [C.c_char_p, _PP, C.c_int32, _PP, C.c_int32, C.POINTER(C.c_int64),
+                                       C.POINTER(C.c_int64), C.c_int32, C.c_int32, C.c_char_p, C.c_int64,
+                                       C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     "oec_selftest_rcp": (C.c_int, [C.c_ulonglong, C.c_ulonglong, C.POINTER(C.c_ulonglong), C.POINTER(C.c_ulonglong)]),
 }
 
@@ -378,6 +383,31 @@ def oec_apply_program(program: str, inputs: Sequence[Field], outputs: Sequence[F
         sc, nsc = None, 0
     _check(lib().oec_apply_program(program.encode(), ins, len(inputs), outs, len(outputs), sc, nsc, _i64(dom_lb),
                                    _i64(dom_ub), variant, _stream(stream)))
+
+
+def oec_program_create(source: str) -> str:
+    """Compile a stencil-language program (include/oec.h) and register it; returns its name."""
+    name = C.c_char_p()
+    _check(lib().oec_program_create(source.encode(), C.byref(name)))
+    return name.value.decode()
+
+
+def oec_program_destroy(program: str):
+    _check(lib().oec_program_destroy(program.encode()))
+
+
+def oec_program_generate(program: str, inputs: Sequence[Field], outputs: Sequence[Field], dom_lb, dom_ub,
+                         variant: int = OEC_VARIANT_AUTO, compile: bool = False) -> Tuple[str, int]:
+    """The CUDA source liboec generates for this call (and, with compile=True, the NVRTC cubin size)."""
+    ins = (_P * len(inputs))(*[f.ptr for f in inputs])
+    outs = (_P * len(outputs))(*[f.ptr for f in outputs])
+    n, cb = C.c_int64(), C.c_int64()
+    _check(lib().oec_program_generate(program.encode(), ins, len(inputs), outs, len(outputs), _i64(dom_lb),
+                                      _i64(dom_ub), variant, 0, None, 0, C.byref(n), None))
+    buf = C.create_string_buffer(n.value + 1)
+    _check(lib().oec_program_generate(program.encode(), ins, len(inputs), outs, len(outputs), _i64(dom_lb),
+                                      _i64(dom_ub), variant, int(compile), buf, n.value + 1, C.byref(n), C.byref(cb)))
+    return buf.value.decode(), cb.value
 
 
 def oec_last_launch_count() -> int:
