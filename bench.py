@@ -434,11 +434,12 @@ def main():
         e2e = e2e_measure(oec, torch, hh, vh, dtr, domain, args.e2e_steps, world)
 
     # ---- remaining suite (evidence for SURVEY §8(a) a7; not part of the step) ----
-    suite_res = levels = f32_res = None
+    suite_res = levels = f32_res = jit_res = None
     if not args.no_suite and world == 1:
         suite_res = suite_measure(oec, torch, domain, l2, peak)
         levels = levels_measure(oec, torch, domain, l2, peak)
         f32_res = f32_measure(oec, torch, domain, l2, peak)
+        jit_res = jit_measure(oec, torch, domain, l2, peak)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -470,6 +471,8 @@ def main():
             res["optimization_levels"] = levels
         if f32_res is not None:
             res["f32"] = f32_res
+        if jit_res is not None:
+            res["jit"] = jit_res
         print(json.dumps(res), flush=True)
     if decomp:
         dist.barrier()
@@ -514,9 +517,11 @@ def e2e_measure(oec, torch, hh, vh, dtr, domain, steps, world):
             "path": "oec_hdiff/oec_vadv with OEC_DEVICE_HOST fields (pinned), staged by liboec, synchronous"}
 
 
-def program_measure(oec, torch, program, domain, l2, peak, variant=0, reps=20, dtype=np.float64):
+def program_measure(oec, torch, program, domain, l2, peak, variant=0, reps=20, dtype=np.float64, run_name=None):
     """us per launch of one program (CUDA graph of R launches over R rotating input sets > 4x L2).
-    dtype=np.float32: the paper's f32 runs; algorithmic bytes scale with the element size."""
+    dtype=np.float32: the paper's f32 runs; algorithmic bytes scale with the element size.
+    run_name: apply this registered program instead (a stencil-language version of `program` with
+    the same argument order, compiled by liboec's JIT)."""
     host = synth.make_inputs(program, domain, seed=0, dtype=dtype)
     spec = synth.PROGRAMS[program]
     sc = [v for _, v in spec.scalars]
@@ -530,13 +535,14 @@ def program_measure(oec, torch, program, domain, l2, peak, variant=0, reps=20, d
     set_bytes = sum(int(np.prod([f.ub[d] - f.lb[d] for d in range(3)])) * f.itemsize for f in s0[0] + s0[1])
     R = max(2, math.ceil(4 * l2 / set_bytes) + 1)
     sets = [s0] + [make() for _ in range(R - 1)]
-    for ins, outs in sets:  # also sizes any library workspace outside the capture
-        oec.oec_apply_program(program, ins, outs, sc, (0, 0, 0), domain, variant)
+    name = run_name or program
+    for ins, outs in sets:  # also sizes any library workspace / compiles JIT kernels outside the capture
+        oec.oec_apply_program(name, ins, outs, sc, (0, 0, 0), domain, variant)
     torch.cuda.synchronize()
     g = torch.cuda.CUDAGraph()
     with torch.cuda.graph(g):
         for ins, outs in sets:
-            oec.oec_apply_program(program, ins, outs, sc, (0, 0, 0), domain, variant)
+            oec.oec_apply_program(name, ins, outs, sc, (0, 0, 0), domain, variant)
     g.replay()
     torch.cuda.synchronize()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -560,6 +566,28 @@ def suite_measure(oec, torch, domain, l2, peak):
 def f32_measure(oec, torch, domain, l2, peak):
     """Every program in binary32 (P:556 evaluates f32 and f64), default kernels."""
     return {p: program_measure(oec, torch, p, domain, l2, peak, dtype=np.float32) for p in synth.ALL_PROGRAMS}
+
+
+def jit_measure(oec, torch, domain, l2, peak):
+    """The stencil-language versions of every stencil program (tests/programs/*.oec), compiled by
+    liboec's JIT (shape inference, inlining / unrolling / original level, size-specialised NVRTC
+    kernels for sm_100a; include/oec.h), at each optimisation level of P:616, next to the
+    hand-written builtin kernel of the same program (bit-identical results: tests/test_gpu_jit.py)."""
+    res = {}
+    pdir = os.path.join(ROOT, "tests", "programs")
+    for fn in sorted(os.listdir(pdir)):
+        program = fn[:-4]
+        with open(os.path.join(pdir, fn)) as f:
+            name = oec.oec_program_create(f.read())
+        try:
+            r = {lvl: program_measure(oec, torch, program, domain, l2, peak, v, run_name=name)
+                 for lvl, v in (("original", 1), ("inline", 2), ("inline_unroll2", 3), ("inline_unroll4", 4))}
+            r["best"] = min(r, key=lambda n: r[n]["us_per_launch"])
+            r["builtin_us_per_launch"] = program_measure(oec, torch, program, domain, l2, peak, 0)["us_per_launch"]
+        finally:
+            oec.oec_program_destroy(name)
+        res[program] = r
+    return res
 
 
 def levels_measure(oec, torch, domain, l2, peak):

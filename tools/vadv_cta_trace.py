@@ -1,0 +1,52 @@
+"""Per-CTA timeline of vadv_sp (VA_TRACE build): start (after griddepcontrol.wait), first TMA chunk
+landed, forward sweep done, backward done -- quantiles over all CTAs, relative to the earliest start.
+
+    OEC_LIB_PATH=tune/liboec_trace.so python tools/vadv_cta_trace.py [--domain 128 128 80]
+"""
+import argparse
+import ctypes as C
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import numpy as np  # noqa: E402
+
+import synth  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--domain", type=int, nargs=3, default=[128, 128, 80])
+    a = ap.parse_args()
+    import torch
+
+    from paper_2005_13014_b200 import oec
+
+    dom = tuple(a.domain)
+    host = synth.make_inputs("vadv", dom, seed=0)
+    sets = []
+    for _ in range(8):
+        ins = [oec.field_from_host(host[s.name]) for s in synth.PROGRAMS["vadv"].inputs]
+        sets.append((ins, [oec.empty_like_domain(dom, fill=0.0)]))
+    for rep in range(3):
+        for r in range(8):
+            oec.oec_apply_program("vadv", sets[r][0], sets[r][1], [0.15], (0, 0, 0), dom)
+        torch.cuda.synchronize()
+    ncta = min(1024, ((dom[0] + 127) // 128) * dom[1])
+    buf = (C.c_ulonglong * (4 * 1024))()
+    oec.lib().oec_debug_vadv_cta(buf)
+    t = np.array(buf[:], dtype=np.int64).reshape(4, 1024)[:, :ncta]
+    t0 = t[0].min()
+    names = ["start", "first chunk", "forward done", "end"]
+    print(f"domain {dom}, {ncta} CTAs; times in us after the earliest CTA start")
+    for e in range(4):
+        q = np.quantile((t[e] - t0) / 1e3, [0, 0.1, 0.5, 0.9, 1.0])
+        print(f"{names[e]:14s} min {q[0]:6.2f}  p10 {q[1]:6.2f}  med {q[2]:6.2f}  p90 {q[3]:6.2f}  max {q[4]:6.2f}")
+    fwd = (t[2] - t[1]) / 1e3
+    bwd = (t[3] - t[2]) / 1e3
+    print(f"forward (first chunk -> done) med {np.median(fwd):.2f} us, backward med {np.median(bwd):.2f} us")
+
+
+if __name__ == "__main__":
+    main()
