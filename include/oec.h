@@ -92,7 +92,11 @@ typedef enum {
                                 producer evaluations computed once.  Not for vadv
                                 (OEC_ERR_UNSUPPORTED: unrolling does not apply to the column
                                 solver)                                                        */
-    OEC_VARIANT_UNROLL4 = 4  /* "inline+unroll(4)": as UNROLL2 with factor 4                    */
+    OEC_VARIANT_UNROLL4 = 4, /* "inline+unroll(4)": as UNROLL2 with factor 4                    */
+    OEC_VARIANT_UNROLL2_K = 5, /* inline + unroll by 2 along k ("the unrolling pass supports all
+                                unroll dimensions"): stencil-language programs only
+                                (oec_program_create); builtins: OEC_ERR_UNSUPPORTED            */
+    OEC_VARIANT_UNROLL4_K = 6  /* as UNROLL2_K with factor 4                                    */
 } oec_variant;
 
 typedef struct oec_field {

@@ -618,12 +618,18 @@ struct Spec {
     int dtype = OEC_F64;
     int variant = OEC_VARIANT_NAIVE;
     int unroll = 1;
+    int unroll_dim = 1;  // 1: j, 2: k
     int n[3] = {0, 0, 0};  // domain size
     std::vector<int32_t> in_sj, in_sk, out_sj, out_sk;
 };
 
 static int unroll_of(int variant) {
-    return variant == OEC_VARIANT_UNROLL2 ? 2 : variant == OEC_VARIANT_UNROLL4 ? 4 : 1;
+    return (variant == OEC_VARIANT_UNROLL2 || variant == OEC_VARIANT_UNROLL2_K)   ? 2
+           : (variant == OEC_VARIANT_UNROLL4 || variant == OEC_VARIANT_UNROLL4_K) ? 4
+                                                                                 : 1;
+}
+static int unroll_dim_of(int variant) {
+    return (variant == OEC_VARIANT_UNROLL2_K || variant == OEC_VARIANT_UNROLL4_K) ? 2 : 1;
 }
 
 // launch geometry of the paper's execution model: one thread per point (U points along j)
@@ -815,46 +821,62 @@ static std::string kernel_params(const Program &P, bool outputs, const std::vect
     return o.str();
 }
 
-// inline / inline+unroll(U): one kernel, every operator inlined into the outputs
+// inline / inline+unroll(U): one kernel, every operator inlined into the outputs.  Unrolling
+// along j (dim 1) or k (dim 2): one thread evaluates U points; operator instances and loads
+// shared between them are emitted once (CSE), e.g. the k+1 plane of a k-unrolled thread.
 static std::string gen_fused(const Program &P, const Spec &S) {
     std::ostringstream o;
-    const int U = S.unroll;
+    const int U = S.unroll, ud = S.unroll_dim;
     int bx, by;
     block_of(S.n, &bx, &by);
-    emit_header(o, P, S, U == 1 ? "inline (P:431)" : ("inline+unroll(" + std::to_string(U) + ") along j (P:447)").c_str());
+    const char *dn = ud == 2 ? "k" : "j";
+    emit_header(o, P, S,
+                U == 1 ? "inline (P:431)"
+                       : ("inline+unroll(" + std::to_string(U) + ") along " + dn + " (P:447-451)").c_str());
     o << "extern \"C\" __global__ void __launch_bounds__(" << bx * by << ") oec_jit_fused("
       << kernel_params(P, true, nullptr, nullptr) << ") {\n"
-      << "    const int i = blockIdx.x * " << bx << " + threadIdx.x;\n"
-      << "    const int j0 = (blockIdx.y * " << by << " + threadIdx.y) * " << U << ";\n"
-      << "    const int k = blockIdx.z;\n"
-      << "    if (i >= " << S.n[0] << " || j0 >= " << S.n[1] << ") return;\n";
-    auto body = [&](int rows, const char *jv) {
+      << "    const int i = blockIdx.x * " << bx << " + threadIdx.x;\n";
+    if (ud == 2)
+        o << "    const int j = blockIdx.y * " << by << " + threadIdx.y;\n"
+          << "    const int k0 = blockIdx.z * " << U << ";\n"
+          << "    if (i >= " << S.n[0] << " || j >= " << S.n[1] << ") return;\n";
+    else
+        o << "    const int j0 = (blockIdx.y * " << by << " + threadIdx.y) * " << U << ";\n"
+          << "    const int k = blockIdx.z;\n"
+          << "    if (i >= " << S.n[0] << " || j0 >= " << S.n[1] << ") return;\n";
+    // rows: points per thread; jv / kv: the first point's j / k expressions
+    auto body = [&](int rows, const char *jv, const char *kv) {
         Emitter E(P, S, false);
         for (size_t q = 0; q < P.in_names.size(); ++q)
             if (P.in_used[q])
                 E.o << E.ind << "const T *__restrict__ b" << q << " = f" << q << " + (i + " << jv << " * " << S.in_sj[q]
-                    << (P.in_kinv[q] ? "" : " + k * " + std::to_string(S.in_sk[q])) << ");\n";
+                    << (P.in_kinv[q] ? std::string() : std::string(" + ") + kv + " * " + std::to_string(S.in_sk[q]))
+                    << ");\n";
         std::vector<std::vector<std::string>> vals(rows);
         for (int u = 0; u < rows; ++u)
             for (size_t q = 0; q < P.out_names.size(); ++q) {
                 int t = P.out_temp[q];
-                int off[3] = {0, u, 0};
+                int off[3] = {0, ud == 1 ? u : 0, ud == 2 ? u : 0};
                 vals[u].push_back(E.temp(t, off));
             }
         // stores after all loads (outputs kept in registers)
         for (int u = 0; u < rows; ++u)
             for (size_t q = 0; q < P.out_names.size(); ++q)
-                E.o << E.ind << "g" << q << "[i + (" << jv << " + " << u << ") * " << S.out_sj[q] << " + k * " << S.out_sk[q]
-                    << "] = " << vals[u][q] << ";\n";
+                E.o << E.ind << "g" << q << "[i + (" << jv << (ud == 1 ? " + " + std::to_string(u) : std::string()) << ") * "
+                    << S.out_sj[q] << " + (" << kv << (ud == 2 ? " + " + std::to_string(u) : std::string()) << ") * "
+                    << S.out_sk[q] << "] = " << vals[u][q] << ";\n";
         return E.o.str();
     };
-    if (S.n[1] % U == 0) {
-        o << "    {\n" << body(U, "j0") << "    }\n";
+    const int N = S.n[ud];
+    const std::string v0 = ud == 2 ? "k0" : "j0";
+    const char *jv = ud == 2 ? "j" : "j0", *kv = ud == 2 ? "k0" : "k";
+    if (N % U == 0) {
+        o << "    {\n" << body(U, jv, kv) << "    }\n";
     } else {
-        o << "    if (j0 + " << U << " <= " << S.n[1] << ") {\n"
-          << body(U, "j0") << "    } else {\n"
-          << "      for (int j = j0; j < " << S.n[1] << "; ++j) {\n"
-          << body(1, "j") << "      }\n    }\n";
+        o << "    if (" << v0 << " + " << U << " <= " << N << ") {\n"
+          << body(U, jv, kv) << "    } else {\n"
+          << "      for (int r = " << v0 << "; r < " << N << "; ++r) {\n"
+          << body(1, ud == 2 ? "j" : "r", ud == 2 ? "r" : "k") << "      }\n    }\n";
     }
     o << "}\n";
     return o.str();
@@ -1056,6 +1078,7 @@ static oec_status make_spec(const Program &P, const oec_field *const *in, oec_fi
     S->dtype = sizeof(T) == 4 ? OEC_F32 : OEC_F64;
     S->variant = variant == OEC_VARIANT_AUTO ? OEC_VARIANT_NAIVE : variant;
     S->unroll = unroll_of(S->variant);
+    S->unroll_dim = unroll_dim_of(S->variant);
     for (int d = 0; d < 3; ++d) S->n[d] = (int)(hi[d] - lo[d]);
     for (size_t q = 0; q < P.in_names.size(); ++q) {
         FVT<T> v;
@@ -1129,8 +1152,8 @@ static oec_status get_compiled(const Program &P, const Spec &S, int device, std:
 }
 
 template <class T>
-static oec_status run(const Program &P, const oec_field *const *in, oec_field *const *out, const double *sc,
-                      const int64_t *lo, const int64_t *hi, int variant, cudaStream_t s) {
+static oec_status run_variant(const Program &P, const oec_field *const *in, oec_field *const *out, const double *sc,
+                              const int64_t *lo, const int64_t *hi, int variant, cudaStream_t s) {
     Spec S;
     std::vector<const T *> pin;
     std::vector<T *> pout;
@@ -1156,7 +1179,8 @@ static oec_status run(const Program &P, const oec_field *const *in, oec_field *c
         for (auto &p : pin) args.push_back((void *)&p);
         for (auto &p : pout) args.push_back((void *)&p);
         for (auto &x : scal) args.push_back((void *)&x);
-        int e[3] = {S.n[0], (S.n[1] + S.unroll - 1) / S.unroll, S.n[2]};
+        int e[3] = {S.n[0], S.n[1], S.n[2]};
+        e[S.unroll_dim] = (e[S.unroll_dim] + S.unroll - 1) / S.unroll;
         if ((st = launch(C->fns[0], e, args))) return st;
     } else {
         size_t total;
@@ -1215,6 +1239,84 @@ static oec_status run(const Program &P, const oec_field *const *in, oec_field *c
     return OEC_OK;
 }
 
+// AUTO: "we thus employ empirical tuning to find the best unroll factor".  The first AUTO
+// call of a (program, dtype, size, strides, device) specialisation times the inline level and
+// unroll(2/4) along j and k on the caller's stream -- every variant gives bit-identical outputs,
+// so the tuning launches are harmless -- with L2 flushed before each timed launch, and caches the
+// fastest.  Inside a stream capture (no synchronisation possible) an untuned specialisation runs
+// the inline level and is not cached.
+struct Tuned {
+    int variant;
+    float us[5];
+};
+static std::map<std::string, Tuned> g_tuned;
+
+template <class T>
+static oec_status run(const Program &P, const oec_field *const *in, oec_field *const *out, const double *sc,
+                      const int64_t *lo, const int64_t *hi, int variant, cudaStream_t s) {
+    if (variant != OEC_VARIANT_AUTO) return run_variant<T>(P, in, out, sc, lo, hi, variant, s);
+    Spec S;
+    oec_status st = make_spec<T>(P, in, out, lo, hi, OEC_VARIANT_NAIVE, &S, nullptr, nullptr);
+    if (st) return st;
+    const int device = in[0]->device;
+    S.variant = -1;  // variant-free key
+    const std::string key = spec_key(P, S, device);
+    int tuned = -1;
+    {
+        std::lock_guard<std::mutex> g(g_mu);  // released before launching (get_compiled locks it)
+        auto it = g_tuned.find(key);
+        if (it != g_tuned.end()) tuned = it->second.variant;
+    }
+    if (tuned >= 0) return run_variant<T>(P, in, out, sc, lo, hi, tuned, s);
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(s, &cap) != cudaSuccess || cap != cudaStreamCaptureStatusNone)
+        return run_variant<T>(P, in, out, sc, lo, hi, OEC_VARIANT_NAIVE, s);
+    static const int cand[5] = {OEC_VARIANT_NAIVE, OEC_VARIANT_UNROLL2, OEC_VARIANT_UNROLL4, OEC_VARIANT_UNROLL2_K,
+                                OEC_VARIANT_UNROLL4_K};
+    int l2 = 0;
+    cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, device);
+    const size_t flush_bytes = (size_t)std::max(l2, 1 << 20) * 2;
+    void *flush = nullptr;
+    if (cudaMalloc(&flush, flush_bytes) != cudaSuccess) flush = nullptr;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    Tuned best{OEC_VARIANT_NAIVE, {0, 0, 0, 0, 0}};
+    float best_us = 1e30f;
+    int launches = 0;
+    for (int c = 0; c < 5; ++c) {
+        if ((st = run_variant<T>(P, in, out, sc, lo, hi, cand[c], s))) break;  // compile + warm
+        float tot = 0.f;
+        for (int rep = 0; rep < 3 && !st; ++rep) {
+            if (flush) cudaMemsetAsync(flush, rep, flush_bytes, s);
+            cudaEventRecord(e0, s);
+            st = run_variant<T>(P, in, out, sc, lo, hi, cand[c], s);
+            cudaEventRecord(e1, s);
+            cudaEventSynchronize(e1);
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, e0, e1);
+            tot += ms;
+        }
+        if (st) break;
+        best.us[c] = 1e3f * tot / 3.f;
+        if (best.us[c] < best_us) {
+            best_us = best.us[c];
+            best.variant = cand[c];
+        }
+        launches += 4;
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (flush) cudaFree(flush);
+    if (st) return st;
+    {
+        std::lock_guard<std::mutex> g(g_mu);
+        g_tuned[key] = best;
+    }
+    set_launch_count(launches);  // the tuning launches (the outputs are theirs)
+    return OEC_OK;
+}
+
 static ProgDesc make_desc(const std::shared_ptr<Registered> &R) {
     const Program &P = R->prog;
     ProgDesc D;
@@ -1226,6 +1328,7 @@ static ProgDesc make_desc(const std::shared_ptr<Registered> &R) {
     D.in_lo = P.in_lo;
     D.in_hi = P.in_hi;
     D.in_kinv = P.in_kinv;
+    D.kunroll_ok = true;
     const Registered *raw = R.get();  // kept alive by the registry / the lookup's shared_ptr
     D.run = [raw](int dtype, const oec_field *const *in, oec_field *const *out, const double *sc, const int64_t *lo,
                   const int64_t *hi, int variant, cudaStream_t s) {
@@ -1304,7 +1407,7 @@ oec_status oec_program_generate(const char *program, const oec_field *const *inp
         n_outputs != (int)P.out_names.size())
         return set_error(OEC_ERR_ARG, "oec_program_generate: %s expects %d inputs / %d outputs", P.name.c_str(),
                          (int)P.in_names.size(), (int)P.out_names.size());
-    if (variant < OEC_VARIANT_AUTO || variant > OEC_VARIANT_UNROLL4)
+    if (variant < OEC_VARIANT_AUTO || variant > OEC_VARIANT_UNROLL4_K)
         return set_error(OEC_ERR_ARG, "oec_program_generate: unknown variant %d", variant);
     int device = -2, dtype = -1;
     for (int q = 0; q < n_inputs; ++q) {

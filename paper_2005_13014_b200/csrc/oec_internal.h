@@ -142,7 +142,8 @@ struct ProgDesc {
     std::vector<int> in_kinv;
     std::vector<double> sc_dflt;
     int min_k = 1;          // smallest K the program accepts (vadv: 2)
-    bool unroll_ok = true;  // OEC_VARIANT_UNROLL2/4 meaningful
+    bool unroll_ok = true;    // OEC_VARIANT_UNROLL2/4 meaningful
+    bool kunroll_ok = false;  // OEC_VARIANT_UNROLL2_K/4_K implemented (stencil-language programs)
     // device runner: called with validated device fields (registry order) and complete scalars
     std::function<oec_status(int dtype, const oec_field *const *in, oec_field *const *out, const double *sc,
                              const int64_t *lo, const int64_t *hi, int variant, cudaStream_t s)>

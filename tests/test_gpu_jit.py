@@ -32,7 +32,7 @@ def _oec():
     return oec
 
 
-VARIANTS = [0, 1, 2, 3, 4]  # AUTO, UNFUSED (original), NAIVE (inline), UNROLL2, UNROLL4
+VARIANTS = [0, 1, 2, 3, 4, 5, 6]  # AUTO (tuned), UNFUSED (original), NAIVE (inline), UNROLL2/4 (j), UNROLL2/4_K
 
 
 def text_of(program):
@@ -90,9 +90,9 @@ def test_text_programs_bit_identical(program, variant, dtype):
     host = synth.make_inputs(program, domain, seed=1, dtype=dtype)
     got, n_launch = run_jit(name, tp, host, domain, variant)
     check(got, oracle(tp, host, (0, 0, 0), domain), (0, 0, 0), domain)
-    if variant != 1:
+    if variant >= 2:
         assert n_launch == 1
-    else:
+    elif variant == 1:
         assert n_launch == len(tp.program.applies)  # one kernel per (live) stencil.apply
 
 
@@ -118,7 +118,7 @@ def test_random_programs_bit_identical(seed):
     host = rnd_inputs(tp, domain, ext, seed=seed)
     name = registered(text)
     ref = oracle(tp, host, (0, 0, 0), domain)
-    for variant in (1, 2, 3, 4):
+    for variant in (1, 2, 3, 4, 5, 6, 0):
         got, _ = run_jit(name, tp, host, domain, variant)
         check(got, ref, (0, 0, 0), domain)
 
@@ -132,7 +132,7 @@ def test_random_programs_f32():
         host = rnd_inputs(tp, domain, ext, seed=seed, dtype=np.float32)
         name = registered(text)
         ref = oracle(tp, host, (0, 0, 0), domain)
-        for variant in (1, 2, 4):
+        for variant in (1, 2, 4, 6):
             got, _ = run_jit(name, tp, host, domain, variant)
             check(got, ref, (0, 0, 0), domain)
 
@@ -190,3 +190,20 @@ def test_graph_capture_after_first_compile():
     ref = oracle(tp, host, (0, 0, 0), domain)
     for o, f in zip(tp.outputs, outs):
         assert np.array_equal(f.download(), ref[o])
+
+
+def test_auto_tuning_is_cached_and_bit_identical():
+    """AUTO = empirical tuning: the first call times the inline / unrolled variants (its
+    outputs come from those launches), later calls launch the cached choice once."""
+    program = "nh_p_grad"
+    name = registered(text_of(program))
+    tp = dsl.parse(text_of(program))
+    domain = (64, 48, 16)
+    host = synth.make_inputs(program, domain, seed=7)
+    ref = oracle(tp, host, (0, 0, 0), domain)
+    got, n1 = run_jit(name, tp, host, domain, 0)
+    check(got, ref, (0, 0, 0), domain)
+    assert n1 == 20  # 5 candidates x (1 warm-up + 3 timed)
+    got, n2 = run_jit(name, tp, host, domain, 0)
+    check(got, ref, (0, 0, 0), domain)
+    assert n2 == 1

@@ -23,7 +23,8 @@ from paper_2005_13014_b200 import oec
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 NAMES = sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(HERE, "programs", "*.oec")))
-VARIANTS = [oec.OEC_VARIANT_NAIVE, oec.OEC_VARIANT_UNROLL2, oec.OEC_VARIANT_UNROLL4, oec.OEC_VARIANT_UNFUSED]
+VARIANTS = [oec.OEC_VARIANT_NAIVE, oec.OEC_VARIANT_UNROLL2, oec.OEC_VARIANT_UNROLL4, oec.OEC_VARIANT_UNFUSED,
+            oec.OEC_VARIANT_UNROLL2_K, oec.OEC_VARIANT_UNROLL4_K]
 
 
 def text_of(program):
@@ -152,7 +153,7 @@ def test_dead_operators_do_not_widen_extents():
 @pytest.mark.parametrize("program", NAMES)
 @pytest.mark.parametrize("variant", VARIANTS)
 def test_generated_source_compiles_for_sm100a(program, variant):
-    domain = (33, 19, 5)  # ragged: 19 rows do not divide by 2 or 4
+    domain = (33, 19, 5)  # ragged: 19 rows / 5 levels do not divide by 2 or 4
     with Registered(text_of(program)) as name:
         ins, outs = host_fields(name, domain)
         src, cubin = oec.oec_program_generate(name, ins, outs, (0, 0, 0), domain, variant, compile=True)
@@ -199,3 +200,23 @@ def test_generate_argument_errors():
         assert _status(lambda: oec.oec_program_generate(name, ins[:2], outs, (0, 0, 0), (8, 8, 2)))[0] == 1
         assert _status(lambda: oec.oec_program_generate(name, ins, outs, (0, 0, 0), (8, 8, 2), variant=9))[0] == 1
     assert _status(lambda: oec.oec_program_generate("hdiff", [], [], (0, 0, 0), (8, 8, 2)))[0] == 1
+
+
+def test_k_unroll_shares_levels():
+    """Unrolling along k (P:451 'all unroll dimensions'): a thread evaluating 4 levels loads each
+    k-offset plane once -- nh_p_grad's gz/pk3/pp k and k+1 accesses are shared between levels."""
+    domain = (32, 16, 8)
+    with Registered(text_of("nh_p_grad")) as name:
+        ins, outs = host_fields(name, domain)
+        src1, _ = oec.oec_program_generate(name, ins, outs, (0, 0, 0), domain, oec.OEC_VARIANT_NAIVE)
+        src4, _ = oec.oec_program_generate(name, ins, outs, (0, 0, 0), domain, oec.OEC_VARIANT_UNROLL4_K)
+        for f in ("b2", "b3", "b4"):  # pp, gz, pk3
+            n1 = len(re.findall(rf"= {f}\[", src1))
+            n4 = len(re.findall(rf"= {f}\[", src4)) / 4
+            assert n4 < n1, (f, n1, n4)
+        assert "k0 = blockIdx.z * 4" in src4
+
+
+def test_k_unroll_rejected_for_builtins():
+    st, msg = _status(lambda: oec.oec_apply_program("uvbke", [], [], None, (0, 0, 0), (8, 8, 2), oec.OEC_VARIANT_UNROLL2_K))
+    assert st in (1, 7)
