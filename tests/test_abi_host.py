@@ -108,7 +108,9 @@ def test_error_arg_counts_and_program():
     inp, cf, out = _hdiff_host_fields()
     assert _status(lambda: oec.oec_apply_program("hdiff", [inp], [out], dom_ub=(8, 8, 2)))[0] == 1
     assert _status(lambda: oec.oec_apply_program("nope", [inp, cf], [out], dom_ub=(8, 8, 2)))[0] == 1
-    assert _status(lambda: oec.oec_apply_program("hdiff", [inp, cf], [out], dom_ub=(8, 8, 2), variant=5))[0] == 1
+    assert _status(lambda: oec.oec_apply_program("hdiff", [inp, cf], [out], dom_ub=(8, 8, 2), variant=9))[0] == 1
+    # unrolling along k exists for stencil-language programs only
+    assert _status(lambda: oec.oec_apply_program("hdiff", [inp, cf], [out], dom_ub=(8, 8, 2), variant=5))[0] == 7
 
 
 def test_unroll_variant_rejected_for_vadv():
