@@ -571,8 +571,9 @@ def f32_measure(oec, torch, domain, l2, peak):
 def jit_measure(oec, torch, domain, l2, peak):
     """The stencil-language versions of every stencil program (tests/programs/*.oec), compiled by
     liboec's JIT (shape inference, inlining / unrolling / original level, size-specialised NVRTC
-    kernels for sm_100a; include/oec.h), at each optimisation level of P:616, next to the
-    hand-written builtin kernel of the same program (bit-identical results: tests/test_gpu_jit.py)."""
+    kernels for sm_100a; include/oec.h), at each optimisation level of P:616 (unrolling along j and
+    k) and AUTO (empirical tuning), next to the hand-written builtin kernel of the same
+    program (bit-identical results: tests/test_gpu_jit.py)."""
     res = {}
     pdir = os.path.join(ROOT, "tests", "programs")
     for fn in sorted(os.listdir(pdir)):
@@ -581,7 +582,9 @@ def jit_measure(oec, torch, domain, l2, peak):
             name = oec.oec_program_create(f.read())
         try:
             r = {lvl: program_measure(oec, torch, program, domain, l2, peak, v, run_name=name)
-                 for lvl, v in (("original", 1), ("inline", 2), ("inline_unroll2", 3), ("inline_unroll4", 4))}
+                 for lvl, v in (("original", 1), ("inline", 2), ("inline_unroll2", 3), ("inline_unroll4", 4),
+                                ("inline_unroll2_k", 5), ("inline_unroll4_k", 6), ("tiled_tma", 7),
+                                ("auto_tuned", 0))}
             r["best"] = min(r, key=lambda n: r[n]["us_per_launch"])
             r["builtin_us_per_launch"] = program_measure(oec, torch, program, domain, l2, peak, 0)["us_per_launch"]
         finally:

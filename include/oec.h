@@ -96,7 +96,12 @@ typedef enum {
     OEC_VARIANT_UNROLL2_K = 5, /* inline + unroll by 2 along k ("the unrolling pass supports all
                                 unroll dimensions"): stencil-language programs only
                                 (oec_program_create); builtins: OEC_ERR_UNSUPPORTED            */
-    OEC_VARIANT_UNROLL4_K = 6  /* as UNROLL2_K with factor 4                                    */
+    OEC_VARIANT_UNROLL4_K = 6, /* as UNROLL2_K with factor 4                                    */
+    OEC_VARIANT_TILED = 7    /* B200 tiling for stencil-language programs: persistent CTAs, each
+                                3D input's tile + access extent staged into a shared-memory ring
+                                by TMA, the inlined expression reads shared memory; inputs must
+                                be TMA-describable (oec_field_create layout) else
+                                OEC_ERR_LAYOUT; builtins: OEC_ERR_UNSUPPORTED                    */
 } oec_variant;
 
 typedef struct oec_field {

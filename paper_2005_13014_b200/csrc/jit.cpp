@@ -623,6 +623,78 @@ struct Spec {
     std::vector<int32_t> in_sj, in_sk, out_sj, out_sk;
 };
 
+// OEC_VARIANT_TILED: the B200 execution model for a stencil-language program.  Persistent CTAs of
+// 256 threads walk items = (64 x 8 tile of (i, j), one k-level); every 3D input's box -- the tile
+// grown by that input's access extent (shape inference) in i, j and k -- is staged into a
+// shared-memory ring by TMA (one elected thread, mbarrier completion), the inlined expression
+// reads shared memory at immediate offsets, k-invariant inputs are read through L1, outputs are
+// stored straight from registers.  S stages keep the next items' boxes in flight while one is
+// computed.
+struct TileLayout {
+    int ti = 64, tj = 8, rows = 2;   // tile, rows per thread (256 threads = ti x (tj / rows))
+    int ntile[3] = {0, 0, 0};        // items per dim (k: one level per item)
+    std::vector<int> staged;         // per input: 1 = TMA box in shared memory
+    std::vector<int> w, h, dpt;      // box extents (i, j, k) per staged input
+    std::vector<int> swap;           // tensor dims ordered (i, k, j) -- shared memory [j][k][i]
+    std::vector<int> off;            // byte offset of the box within a stage
+    std::vector<int32_t> ssj, ssk;   // shared-memory strides (elements)
+    int stage_bytes = 0, stages = 2, smem = 0;
+    int stage_bytes_tx(int esz) const {  // bytes the boxes of one stage deliver (complete_tx count)
+        int b = 0;
+        for (size_t q = 0; q < staged.size(); ++q)
+            if (staged[q]) b += w[q] * h[q] * dpt[q] * esz;
+        return b;
+    }
+};
+
+static TileLayout tile_layout(const Program &P, const Spec &S, int esz) {
+    TileLayout L;
+    L.ti = S.n[0] >= 64 ? 64 : 32;
+    L.rows = 2;
+    L.tj = (256 / L.ti) * L.rows;
+    L.ntile[0] = (S.n[0] + L.ti - 1) / L.ti;
+    L.ntile[1] = (S.n[1] + L.tj - 1) / L.tj;
+    L.ntile[2] = S.n[2];
+    const int nin = (int)P.in_names.size();
+    L.staged.assign(nin, 0);
+    L.w.assign(nin, 0);
+    L.h.assign(nin, 0);
+    L.dpt.assign(nin, 0);
+    L.swap.assign(nin, 0);
+    L.off.assign(nin, 0);
+    L.ssj.assign(nin, 0);
+    L.ssk.assign(nin, 0);
+    int at = 0;
+    for (int q = 0; q < nin; ++q) {
+        if (!P.in_used[q] || P.in_kinv[q]) continue;
+        L.staged[q] = 1;
+        int w = L.ti + P.in_hi[q][0] - P.in_lo[q][0];
+        // the box starts on a 16-byte boundary (a misaligned start faults with an illegal
+        // instruction, measured on B200): up to 16/esz - 1 extra leading columns, whose count (the
+        // shift) is a launch argument; inner extent a multiple of 16 bytes
+        const int per16 = 16 / esz;
+        w = (w + per16 - 1 + per16 - 1) / per16 * per16;
+        L.w[q] = w;
+        L.h[q] = L.tj + P.in_hi[q][1] - P.in_lo[q][1];
+        L.dpt[q] = 1 + P.in_hi[q][2] - P.in_lo[q][2];
+        L.swap[q] = S.in_sk[q] < S.in_sj[q];
+        if (L.swap[q]) {  // shared memory [j][k][i]
+            L.ssk[q] = w;
+            L.ssj[q] = w * L.dpt[q];
+        } else {  // [k][j][i]
+            L.ssj[q] = w;
+            L.ssk[q] = w * L.h[q];
+        }
+        L.off[q] = at;
+        at += (w * L.h[q] * L.dpt[q] * esz + 127) / 128 * 128;
+    }
+    L.stage_bytes = at;
+    // 2..4 stages, at most ~110 KB per CTA so two CTAs share an SM
+    L.stages = at > 0 ? std::max(2, std::min(4, (110 * 1024) / std::max(at, 1))) : 1;
+    L.smem = L.stages * at + 8 * L.stages + 16;
+    return L;
+}
+
 static int unroll_of(int variant) {
     return (variant == OEC_VARIANT_UNROLL2 || variant == OEC_VARIANT_UNROLL2_K)   ? 2
            : (variant == OEC_VARIANT_UNROLL4 || variant == OEC_VARIANT_UNROLL4_K) ? 4
@@ -1017,6 +1089,7 @@ struct Drv {
     PFN_cuModuleLoadData_v2000 load = nullptr;
     PFN_cuModuleGetFunction_v2000 get = nullptr;
     PFN_cuLaunchKernel_v4000 launch = nullptr;
+    PFN_cuFuncSetAttribute_v9000 set_attr = nullptr;
 };
 static Drv g_drv;
 static std::once_flag g_drv_once;
@@ -1029,13 +1102,16 @@ static void load_drv() {
         g_drv.get = (PFN_cuModuleGetFunction_v2000)f;
     if (cudaGetDriverEntryPoint("cuLaunchKernel", &f, cudaEnableDefault, &q) == cudaSuccess && q == cudaDriverEntryPointSuccess)
         g_drv.launch = (PFN_cuLaunchKernel_v4000)f;
-    g_drv.ok = g_drv.load && g_drv.get && g_drv.launch;
+    if (cudaGetDriverEntryPoint("cuFuncSetAttribute", &f, cudaEnableDefault, &q) == cudaSuccess && q == cudaDriverEntryPointSuccess)
+        g_drv.set_attr = (PFN_cuFuncSetAttribute_v9000)f;
+    g_drv.ok = g_drv.load && g_drv.get && g_drv.launch && g_drv.set_attr;
 }
 
 // ---------------------------------------------------------------------------------------------
 // registry, kernel cache, runner
 // ---------------------------------------------------------------------------------------------
 struct Compiled {
+    bool attr_set = false;  // dynamic shared-memory limit raised (tiled kernels)
     std::vector<CUfunction> fns;
     std::vector<int> ops;  // original level: operator of each kernel
 };
@@ -1062,7 +1138,133 @@ static std::string spec_key(const Program &P, const Spec &S, int device) {
     return k.str();
 }
 
+
+static const char *TMA_PRELUDE = R"(
+struct __align__(64) TM { unsigned long long v[16]; };
+__device__ __forceinline__ unsigned su32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mb_init(unsigned long long *b, unsigned c) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(c) : "memory"); }
+__device__ __forceinline__ void mb_expect(unsigned long long *b, unsigned n) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(n) : "memory"); }
+__device__ __forceinline__ void mb_wait(unsigned long long *b, unsigned ph) {
+    asm volatile("{\n.reg .pred p;\nW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n@!p bra W_%=;\n}\n"
+                 ::"r"(su32(b)), "r"(ph) : "memory"); }
+__device__ __forceinline__ void tma3(void *dst, const TM *m, unsigned long long *b, int c0, int c1, int c2) {
+    asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];"
+                 ::"r"(su32(dst)), "l"((unsigned long long)m), "r"(su32(b)), "r"(c0), "r"(c1), "r"(c2) : "memory"); }
+)";
+
+static std::string gen_tiled(const Program &P, const Spec &S) {
+    const int esz = S.dtype == OEC_F32 ? 4 : 8;
+    const TileLayout L = tile_layout(P, S, esz);
+    std::ostringstream o;
+    emit_header(o, P, S, "B200 tiled: TMA-staged input boxes in a shared-memory ring, persistent CTAs");
+    o << TMA_PRELUDE;
+    // parameters: tensor maps + base coordinates of staged inputs, pointers of the others
+    std::ostringstream prm;
+    const char *sep = "";
+    for (size_t q = 0; q < P.in_names.size(); ++q) {
+        if (L.staged[q])
+            prm << sep << "const __grid_constant__ TM tm" << q << ", const int c" << q << "x, const int c" << q << "y, const int c" << q
+                << "z, const int h" << q;
+        else
+            prm << sep << "const T *__restrict__ f" << q;
+        sep = ", ";
+    }
+    for (size_t q = 0; q < P.out_names.size(); ++q) prm << sep << "T *__restrict__ g" << q;
+    for (size_t q = 0; q < P.sc_names.size(); ++q) prm << sep << "const T s" << q;
+    const int NI = L.ntile[0] * L.ntile[1] * L.ntile[2];
+    o << "extern \"C\" __global__ void __launch_bounds__(256) oec_jit_tiled(" << prm.str() << ") {\n"
+      << "    extern __shared__ __align__(128) unsigned char smem[];\n"
+      << "    unsigned long long *full = reinterpret_cast<unsigned long long *>(smem + " << L.stages * L.stage_bytes << ");\n"
+      << "    const int tid = threadIdx.x, tx = tid % " << L.ti << ", ty = tid / " << L.ti << ";\n"
+      << "    const int NITEMS = " << NI << ";\n";
+    // TMA issue of one item's boxes into stage `st`, emitted inline where it is used (a lambda
+    // capturing the __grid_constant__ tensor maps would not keep their param-space addresses)
+    auto issue = [&](const std::string &ind, const std::string &item, const std::string &st) {
+        std::ostringstream w;
+        w << ind << "{\n"
+          << ind << "    const int it_ = " << item << ", st_ = " << st << ";\n"
+          << ind << "    const int ti_ = it_ % " << L.ntile[0] << ", tj_ = (it_ / " << L.ntile[0] << ") % " << L.ntile[1]
+          << ", k_ = it_ / " << L.ntile[0] * L.ntile[1] << ";\n"
+          << ind << "    const int i0_ = ti_ * " << L.ti << ", j0_ = tj_ * " << L.tj << ";\n"
+          << ind << "    mb_expect(&full[st_], " << L.stage_bytes_tx(esz) << ");\n";
+        for (size_t q = 0; q < P.in_names.size(); ++q) {
+            if (!L.staged[q]) continue;
+            const std::string cq = "c" + std::to_string(q);
+            w << ind << "    tma3(smem + st_ * " << L.stage_bytes << " + " << L.off[q] << ", &tm" << q << ", &full[st_], "
+              << cq << "x + i0_, " << (L.swap[q] ? cq + "z + k_, " + cq + "y + j0_" : cq + "y + j0_, " + cq + "z + k_")
+              << ");\n";
+        }
+        w << ind << "}\n";
+        return w.str();
+    };
+    o << "    if (tid == 0) {\n"
+      << "        for (int s = 0; s < " << L.stages << "; ++s) mb_init(&full[s], 1);\n"
+      << "        asm volatile(\"fence.mbarrier_init.release.cluster;\" ::: \"memory\");\n"
+      << "        for (int s = 0; s < " << L.stages << "; ++s)\n"
+      << "            if (blockIdx.x + s * gridDim.x < NITEMS)\n"
+      << issue("            ", "blockIdx.x + s * gridDim.x", "s")
+      << "    }\n"
+      << "    __syncthreads();\n"
+      << "    for (int n = 0;; ++n) {\n"
+      << "        const int item = blockIdx.x + n * gridDim.x;\n"
+      << "        if (item >= NITEMS) break;\n"
+      << "        const int st = n % " << L.stages << ";\n"
+      << "        mb_wait(&full[st], (n / " << L.stages << ") & 1);\n"
+      << "        const int ti = item % " << L.ntile[0] << ", tj = (item / " << L.ntile[0] << ") % " << L.ntile[1]
+      << ", k = item / " << L.ntile[0] * L.ntile[1] << ";\n"
+      << "        const int i = ti * " << L.ti << " + tx, jr = ty * " << L.rows << ", j = tj * " << L.tj << " + jr;\n"
+      << "        {\n";
+    // expression body: staged inputs read shared memory with shared-memory strides
+    Spec SS = S;
+    for (size_t q = 0; q < P.in_names.size(); ++q)
+        if (L.staged[q]) {
+            SS.in_sj[q] = L.ssj[q];
+            SS.in_sk[q] = L.ssk[q];
+        }
+    Emitter E(P, SS, false);
+    E.ind = "            ";
+    for (size_t q = 0; q < P.in_names.size(); ++q) {
+        if (!P.in_used[q]) continue;
+        if (L.staged[q])
+            E.o << E.ind << "const T *b" << q << " = reinterpret_cast<const T *>(smem + st * " << L.stage_bytes << " + "
+                << L.off[q] << ") + ((tx - " << P.in_lo[q][0] << " + h" << q << ") + (jr - " << P.in_lo[q][1] << ") * " << L.ssj[q]
+                << " + (" << -P.in_lo[q][2] << ") * " << L.ssk[q] << ");\n";
+        else
+            E.o << E.ind << "const T *__restrict__ b" << q << " = f" << q << " + (i + j * " << S.in_sj[q]
+                << (P.in_kinv[q] ? std::string() : " + k * " + std::to_string(S.in_sk[q])) << ");\n";
+    }
+    std::vector<std::vector<std::string>> vals(L.rows);
+    for (int u = 0; u < L.rows; ++u)
+        for (size_t q = 0; q < P.out_names.size(); ++q) {
+            int off[3] = {0, u, 0};
+            vals[u].push_back(E.temp(P.out_temp[q], off));
+        }
+    for (int u = 0; u < L.rows; ++u) {
+        E.o << E.ind << "if (i < " << S.n[0] << " && j + " << u << " < " << S.n[1] << ") {\n";
+        for (size_t q = 0; q < P.out_names.size(); ++q)
+            E.o << E.ind << "    g" << q << "[i + (j + " << u << ") * " << S.out_sj[q] << " + k * " << S.out_sk[q]
+                << "] = " << vals[u][q] << ";\n";
+        E.o << E.ind << "}\n";
+    }
+    o << E.o.str()
+      << "        }\n"
+      << "        __syncthreads();  // every thread is done with stage st\n"
+      << "        if (tid == 0) {\n"
+      << "            const int nxt = item + " << L.stages << " * gridDim.x;\n"
+      << "            if (nxt < NITEMS) {\n"
+      << "                asm volatile(\"fence.proxy.async.shared::cta;\" ::: \"memory\");\n"
+      << issue("                ", "nxt", "st")
+      << "            }\n"
+      << "        }\n"
+      << "    }\n"
+      << "}\n";
+    return o.str();
+}
+
 static std::string generate(const Program &P, const Spec &S, std::vector<int> *ops) {
+    if (S.variant == OEC_VARIANT_TILED) return gen_tiled(P, S);
     if (S.variant == OEC_VARIANT_UNFUSED) {
         size_t total;
         auto L = temp_layouts(P, S, &total);
@@ -1074,7 +1276,7 @@ static std::string generate(const Program &P, const Spec &S, std::vector<int> *o
 template <class T>
 static oec_status make_spec(const Program &P, const oec_field *const *in, oec_field *const *out, const int64_t *lo,
                             const int64_t *hi, int variant, Spec *S, std::vector<const T *> *pin,
-                            std::vector<T *> *pout) {
+                            std::vector<T *> *pout, bool with_outputs = true) {
     S->dtype = sizeof(T) == 4 ? OEC_F32 : OEC_F64;
     S->variant = variant == OEC_VARIANT_AUTO ? OEC_VARIANT_NAIVE : variant;
     S->unroll = unroll_of(S->variant);
@@ -1088,7 +1290,7 @@ static oec_status make_spec(const Program &P, const oec_field *const *in, oec_fi
         S->in_sk.push_back(v.sk);
         if (pin) pin->push_back(v.p + (lo[0] + lo[1] * (int64_t)v.sj + lo[2] * (int64_t)v.sk));
     }
-    for (size_t q = 0; q < P.out_names.size(); ++q) {
+    for (size_t q = 0; q < P.out_names.size() && with_outputs; ++q) {
         FOT<T> v;
         oec_status st = field_view(out[q], P.out_names[q].c_str(), &v);
         if (st) return st;
@@ -1139,7 +1341,8 @@ static oec_status get_compiled(const Program &P, const Spec &S, int device, std:
         }
     } else {
         CUfunction f;
-        if ((r = g_drv.get(&f, mod, "oec_jit_fused")) != CUDA_SUCCESS)
+        const char *kn = S.variant == OEC_VARIANT_TILED ? "oec_jit_tiled" : "oec_jit_fused";
+        if ((r = g_drv.get(&f, mod, kn)) != CUDA_SUCCESS)
             return set_error(OEC_ERR_CUDA, "%s: cuModuleGetFunction failed (%d)", P.name.c_str(), (int)r);
         C->fns.push_back(f);
     }
@@ -1174,7 +1377,57 @@ static oec_status run_variant(const Program &P, const oec_field *const *in, oec_
         ++launches;
         return OEC_OK;
     };
-    if (S.variant != OEC_VARIANT_UNFUSED) {
+    if (S.variant == OEC_VARIANT_TILED) {
+        const int esz = (int)sizeof(T);
+        const TileLayout L = tile_layout(P, S, esz);
+        if (L.smem > 227 * 1024)
+            return set_error(OEC_ERR_UNSUPPORTED, "%s: OEC_VARIANT_TILED needs %d bytes of shared memory for two stages "
+                             "of the input boxes (> 227 KB: access extents too wide)", P.name.c_str(), L.smem);
+        const int nin = (int)P.in_names.size();
+        constexpr int MAXIN = 32;
+        if (nin > MAXIN) return set_error(OEC_ERR_UNSUPPORTED, "%s: OEC_VARIANT_TILED supports up to %d inputs", P.name.c_str(), MAXIN);
+        alignas(64) TMap tm[MAXIN];  // cuTensorMapEncodeTiled needs 64-byte aligned descriptors
+        std::vector<std::array<int, 4>> cb(nin);
+        std::vector<void *> args;
+        for (int q = 0; q < nin; ++q) {
+            if (!L.staged[q]) {
+                args.push_back((void *)&pin[q]);
+                continue;
+            }
+            const int box[3] = {L.w[q], L.h[q], L.dpt[q]};
+            if (!make_tmap(in[q], box, &tm[q]))
+                return set_error(OEC_ERR_LAYOUT, "%s: input %s cannot be described to TMA (OEC_VARIANT_TILED needs "
+                                 "16-byte aligned rows and strides, e.g. oec_field_create)", P.name.c_str(),
+                                 P.in_names[q].c_str());
+            const int cx = (int)(lo[0] + P.in_lo[q][0]) - tm[q].lb0 + tm[q].ioff, per16 = 16 / esz;
+            const int cxa = cx >= 0 ? cx / per16 * per16 : -((-cx + per16 - 1) / per16) * per16;  // round down
+            cb[q][0] = cxa;
+            cb[q][1] = (int)(lo[1] + P.in_lo[q][1]) - tm[q].lb1;
+            cb[q][2] = (int)(lo[2] + P.in_lo[q][2]) - tm[q].lb2;
+            cb[q][3] = cx - cxa;  // leading columns before the box's first needed column
+            args.push_back((void *)&tm[q].map);
+            args.push_back((void *)&cb[q][0]);
+            args.push_back((void *)&cb[q][1]);
+            args.push_back((void *)&cb[q][2]);
+            args.push_back((void *)&cb[q][3]);
+        }
+        for (auto &p : pout) args.push_back((void *)&p);
+        for (auto &x : scal) args.push_back((void *)&x);
+        if (!C->attr_set) {
+            CUresult r = g_drv.set_attr(C->fns[0], CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, L.smem);
+            if (r != CUDA_SUCCESS) return set_error(OEC_ERR_CUDA, "%s: cuFuncSetAttribute failed (%d)", P.name.c_str(), (int)r);
+            C->attr_set = true;
+        }
+        static int sms = 0;
+        if (!sms && (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess || sms <= 0))
+            sms = 148;
+        const long long nitems = (long long)L.ntile[0] * L.ntile[1] * L.ntile[2];
+        const int bps = std::max(1, std::min(8, (228 * 1024) / (L.smem + 1024)));
+        const unsigned grid = (unsigned)std::max<long long>(1, std::min<long long>(nitems, (long long)sms * bps));
+        CUresult r = g_drv.launch(C->fns[0], grid, 1, 1, 256, 1, 1, (unsigned)L.smem, (CUstream)s, args.data(), nullptr);
+        if (r != CUDA_SUCCESS) return set_error(OEC_ERR_CUDA, "%s: cuLaunchKernel (tiled) failed (%d)", P.name.c_str(), (int)r);
+        ++launches;
+    } else if (S.variant != OEC_VARIANT_UNFUSED) {
         std::vector<void *> args;
         for (auto &p : pin) args.push_back((void *)&p);
         for (auto &p : pout) args.push_back((void *)&p);
@@ -1245,9 +1498,26 @@ static oec_status run_variant(const Program &P, const oec_field *const *in, oec_
 // so the tuning launches are harmless -- with L2 flushed before each timed launch, and caches the
 // fastest.  Inside a stream capture (no synchronisation possible) an untuned specialisation runs
 // the inline level and is not cached.
+// every staged input describable to TMA (and at least one staged input)
+template <class T>
+static bool tiled_possible(const Program &P, const oec_field *const *in, const int64_t *lo, const int64_t *hi) {
+    Spec S;
+    if (make_spec<T>(P, in, nullptr, lo, hi, OEC_VARIANT_TILED, &S, nullptr, nullptr, false)) return false;
+    const TileLayout L = tile_layout(P, S, (int)sizeof(T));
+    int n = 0;
+    for (size_t q = 0; q < P.in_names.size(); ++q) {
+        if (!L.staged[q]) continue;
+        ++n;
+        TMap tm;
+        const int box[3] = {L.w[q], L.h[q], L.dpt[q]};
+        if (!make_tmap(in[q], box, &tm)) return false;
+    }
+    return n > 0 && L.smem <= 227 * 1024;
+}
+
 struct Tuned {
     int variant;
-    float us[5];
+    float us[6];
 };
 static std::map<std::string, Tuned> g_tuned;
 
@@ -1271,8 +1541,8 @@ static oec_status run(const Program &P, const oec_field *const *in, oec_field *c
     cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
     if (cudaStreamIsCapturing(s, &cap) != cudaSuccess || cap != cudaStreamCaptureStatusNone)
         return run_variant<T>(P, in, out, sc, lo, hi, OEC_VARIANT_NAIVE, s);
-    static const int cand[5] = {OEC_VARIANT_NAIVE, OEC_VARIANT_UNROLL2, OEC_VARIANT_UNROLL4, OEC_VARIANT_UNROLL2_K,
-                                OEC_VARIANT_UNROLL4_K};
+    static const int cand[6] = {OEC_VARIANT_NAIVE, OEC_VARIANT_UNROLL2, OEC_VARIANT_UNROLL4, OEC_VARIANT_UNROLL2_K,
+                                OEC_VARIANT_UNROLL4_K, OEC_VARIANT_TILED};
     int l2 = 0;
     cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, device);
     const size_t flush_bytes = (size_t)std::max(l2, 1 << 20) * 2;
@@ -1281,10 +1551,14 @@ static oec_status run(const Program &P, const oec_field *const *in, oec_field *c
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
-    Tuned best{OEC_VARIANT_NAIVE, {0, 0, 0, 0, 0}};
+    Tuned best{OEC_VARIANT_NAIVE, {0, 0, 0, 0, 0, 0}};
     float best_us = 1e30f;
     int launches = 0;
-    for (int c = 0; c < 5; ++c) {
+    for (int c = 0; c < 6; ++c) {
+        if (cand[c] == OEC_VARIANT_TILED && !tiled_possible<T>(P, in, lo, hi)) {
+            best.us[c] = -1.f;  // not describable to TMA: not a candidate
+            continue;
+        }
         if ((st = run_variant<T>(P, in, out, sc, lo, hi, cand[c], s))) break;  // compile + warm
         float tot = 0.f;
         for (int rep = 0; rep < 3 && !st; ++rep) {
@@ -1407,7 +1681,7 @@ oec_status oec_program_generate(const char *program, const oec_field *const *inp
         n_outputs != (int)P.out_names.size())
         return set_error(OEC_ERR_ARG, "oec_program_generate: %s expects %d inputs / %d outputs", P.name.c_str(),
                          (int)P.in_names.size(), (int)P.out_names.size());
-    if (variant < OEC_VARIANT_AUTO || variant > OEC_VARIANT_UNROLL4_K)
+    if (variant < OEC_VARIANT_AUTO || variant > OEC_VARIANT_TILED)
         return set_error(OEC_ERR_ARG, "oec_program_generate: unknown variant %d", variant);
     int device = -2, dtype = -1;
     for (int q = 0; q < n_inputs; ++q) {

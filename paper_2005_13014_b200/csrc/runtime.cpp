@@ -452,12 +452,13 @@ static oec_status apply(const ProgDesc &P, const oec_field *const *in, int n_in,
     if (!in || !out) return set_error(OEC_ERR_ARG, "%s: NULL input/output array", pname);
     if (n_sc != 0 && n_sc != P_n_sc) return set_error(OEC_ERR_ARG, "%s: expects %d scalars, got %d", pname, P_n_sc, n_sc);
     if (n_sc && !scalars) return set_error(OEC_ERR_ARG, "%s: NULL scalars", pname);
-    if (variant < OEC_VARIANT_AUTO || variant > OEC_VARIANT_UNROLL4_K)
+    if (variant < OEC_VARIANT_AUTO || variant > OEC_VARIANT_TILED)
         return set_error(OEC_ERR_ARG, "%s: unknown variant %d", pname, variant);
-    if ((variant == OEC_VARIANT_UNROLL2_K || variant == OEC_VARIANT_UNROLL4_K) && !P.kunroll_ok)
+    if ((variant == OEC_VARIANT_UNROLL2_K || variant == OEC_VARIANT_UNROLL4_K || variant == OEC_VARIANT_TILED) &&
+        !P.kunroll_ok)
         return set_error(OEC_ERR_UNSUPPORTED,
-                         "%s: unrolling along k is implemented for stencil-language programs (oec_program_create)",
-                         pname);
+                         "%s: unrolling along k and the tiled variant are implemented for stencil-language programs "
+                         "(oec_program_create)", pname);
     if ((variant == OEC_VARIANT_UNROLL2 || variant == OEC_VARIANT_UNROLL4) && !P.unroll_ok)
         return set_error(OEC_ERR_UNSUPPORTED,
                          "%s: stencil unrolling (P:447) does not apply to the vertical solver (independent columns, "

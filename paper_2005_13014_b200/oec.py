@@ -30,6 +30,7 @@ OEC_VARIANT_UNROLL2 = 3
 OEC_VARIANT_UNROLL4 = 4
 OEC_VARIANT_UNROLL2_K = 5
 OEC_VARIANT_UNROLL4_K = 6
+OEC_VARIANT_TILED = 7
 STATUS = {0: "OK", 1: "ERR_ARG", 2: "ERR_SHAPE", 3: "ERR_ALIAS", 4: "ERR_DTYPE", 5: "ERR_CUDA", 6: "ERR_NCCL",
           7: "ERR_UNSUPPORTED", 8: "ERR_LAYOUT"}
 

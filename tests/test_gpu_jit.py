@@ -32,7 +32,7 @@ def _oec():
     return oec
 
 
-VARIANTS = [0, 1, 2, 3, 4, 5, 6]  # AUTO (tuned), UNFUSED (original), NAIVE (inline), UNROLL2/4 (j), UNROLL2/4_K
+VARIANTS = [0, 1, 2, 3, 4, 5, 6, 7]  # AUTO (tuned), UNFUSED (original), NAIVE (inline), UNROLL2/4 (j), UNROLL2/4_K, TILED
 
 
 def text_of(program):
@@ -97,6 +97,19 @@ def test_text_programs_bit_identical(program, variant, dtype):
 
 
 @pytest.mark.parametrize("program", NAMES)
+@pytest.mark.parametrize("domain", [(128, 128, 80), (200, 70, 9)])
+def test_tiled_variant_large_and_ragged(program, domain):
+    """OEC_VARIANT_TILED over many items per CTA (128x128x80) and ragged tiles (200 = 3x64 + 8,
+    70 = 8x8 + 6), bit-identical to the oracle."""
+    name = registered(text_of(program))
+    tp = dsl.parse(text_of(program))
+    host = synth.make_inputs(program, domain, seed=11)
+    got, n = run_jit(name, tp, host, domain, 7)
+    assert n == 1
+    check(got, oracle(tp, host, (0, 0, 0), domain), (0, 0, 0), domain)
+
+
+@pytest.mark.parametrize("program", NAMES)
 def test_text_programs_equal_builtin_kernels(program):
     """JIT of the language version == the hand-written B200 kernel (AUTO) at 128x128x80 (configs[2])."""
     name = registered(text_of(program))
@@ -118,8 +131,12 @@ def test_random_programs_bit_identical(seed):
     host = rnd_inputs(tp, domain, ext, seed=seed)
     name = registered(text)
     ref = oracle(tp, host, (0, 0, 0), domain)
-    for variant in (1, 2, 3, 4, 5, 6, 0):
-        got, _ = run_jit(name, tp, host, domain, variant)
+    for variant in (1, 2, 3, 4, 5, 6, 7, 0):
+        try:
+            got, _ = run_jit(name, tp, host, domain, variant)
+        except Exception as e:  # TILED: boxes of very wide extents may not fit shared memory
+            assert variant == 7 and getattr(e, "status", None) == 7, e
+            continue
         check(got, ref, (0, 0, 0), domain)
 
 
@@ -132,8 +149,12 @@ def test_random_programs_f32():
         host = rnd_inputs(tp, domain, ext, seed=seed, dtype=np.float32)
         name = registered(text)
         ref = oracle(tp, host, (0, 0, 0), domain)
-        for variant in (1, 2, 4, 6):
-            got, _ = run_jit(name, tp, host, domain, variant)
+        for variant in (1, 2, 4, 6, 7):
+            try:
+                got, _ = run_jit(name, tp, host, domain, variant)
+            except Exception as e:
+                assert variant == 7 and getattr(e, "status", None) == 7, e
+                continue
             check(got, ref, (0, 0, 0), domain)
 
 
@@ -203,7 +224,7 @@ def test_auto_tuning_is_cached_and_bit_identical():
     ref = oracle(tp, host, (0, 0, 0), domain)
     got, n1 = run_jit(name, tp, host, domain, 0)
     check(got, ref, (0, 0, 0), domain)
-    assert n1 == 20  # 5 candidates x (1 warm-up + 3 timed)
+    assert n1 == 24  # 6 candidates x (1 warm-up + 3 timed)
     got, n2 = run_jit(name, tp, host, domain, 0)
     check(got, ref, (0, 0, 0), domain)
     assert n2 == 1
