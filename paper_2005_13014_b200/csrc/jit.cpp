@@ -619,6 +619,7 @@ struct Spec {
     int variant = OEC_VARIANT_NAIVE;
     int unroll = 1;
     int unroll_dim = 1;  // 1: j, 2: k
+    int tile_cfg = 0;    // OEC_VARIANT_TILED: index into TILE_CFGS
     int n[3] = {0, 0, 0};  // domain size
     std::vector<int32_t> in_sj, in_sk, out_sj, out_sk;
 };
@@ -647,10 +648,17 @@ struct TileLayout {
     }
 };
 
+// tiled configurations (rows per thread, shared-memory budget per CTA in KB): fewer rows and a
+// smaller ring give more resident CTAs (latency hiding), more rows share loads between rows;
+// AUTO tries them all, OEC_VARIANT_TILED uses the first (measured best on most of the suite).
+static const int TILE_CFGS[][2] = {{1, 56}, {1, 36}, {2, 110}, {4, 110}};
+static const int N_TILE_CFGS = 4;
+
 static TileLayout tile_layout(const Program &P, const Spec &S, int esz) {
     TileLayout L;
+    L.rows = TILE_CFGS[S.tile_cfg][0];
+    const int cta_kb = TILE_CFGS[S.tile_cfg][1];
     L.ti = S.n[0] >= 64 ? 64 : 32;
-    L.rows = 2;
     L.tj = (256 / L.ti) * L.rows;
     L.ntile[0] = (S.n[0] + L.ti - 1) / L.ti;
     L.ntile[1] = (S.n[1] + L.tj - 1) / L.tj;
@@ -690,7 +698,7 @@ static TileLayout tile_layout(const Program &P, const Spec &S, int esz) {
     }
     L.stage_bytes = at;
     // 2..4 stages, at most ~110 KB per CTA so two CTAs share an SM
-    L.stages = at > 0 ? std::max(2, std::min(4, (110 * 1024) / std::max(at, 1))) : 1;
+    L.stages = at > 0 ? std::max(2, std::min(4, (cta_kb * 1024) / std::max(at, 1))) : 1;
     L.smem = L.stages * at + 8 * L.stages + 16;
     return L;
 }
@@ -1131,6 +1139,7 @@ static std::map<int, Workspace> g_ws;  // per device (original level temporaries
 
 static std::string spec_key(const Program &P, const Spec &S, int device) {
     std::ostringstream k;
+    if (S.variant == OEC_VARIANT_TILED) k << "tile" << S.tile_cfg << "|";
     k << P.name << "#" << P.uid << "|d" << device << "|t" << S.dtype << "|v" << S.variant << "|n" << S.n[0] << "," << S.n[1]
       << "," << S.n[2];
     for (size_t q = 0; q < S.in_sj.size(); ++q) k << "|i" << S.in_sj[q] << "," << S.in_sk[q];
@@ -1356,12 +1365,17 @@ static oec_status get_compiled(const Program &P, const Spec &S, int device, std:
 
 template <class T>
 static oec_status run_variant(const Program &P, const oec_field *const *in, oec_field *const *out, const double *sc,
-                              const int64_t *lo, const int64_t *hi, int variant, cudaStream_t s) {
+                              const int64_t *lo, const int64_t *hi, int variant, cudaStream_t s, int tile_cfg = 0) {
     Spec S;
     std::vector<const T *> pin;
     std::vector<T *> pout;
     oec_status st = make_spec<T>(P, in, out, lo, hi, variant, &S, &pin, &pout);
     if (st) return st;
+    if (variant == OEC_VARIANT_TILED && tile_cfg == 0) {  // test hook: force a tiled configuration
+        const char *e = getenv("OEC_JIT_TILE_CFG");
+        if (e && atoi(e) > 0 && atoi(e) < N_TILE_CFGS) tile_cfg = atoi(e);
+    }
+    S.tile_cfg = tile_cfg;
     int device = in[0]->device;
     std::shared_ptr<Compiled> C;
     if ((st = get_compiled(P, S, device, &C))) return st;
@@ -1500,9 +1514,11 @@ static oec_status run_variant(const Program &P, const oec_field *const *in, oec_
 // the inline level and is not cached.
 // every staged input describable to TMA (and at least one staged input)
 template <class T>
-static bool tiled_possible(const Program &P, const oec_field *const *in, const int64_t *lo, const int64_t *hi) {
+static bool tiled_possible(const Program &P, const oec_field *const *in, const int64_t *lo, const int64_t *hi,
+                           int tile_cfg) {
     Spec S;
     if (make_spec<T>(P, in, nullptr, lo, hi, OEC_VARIANT_TILED, &S, nullptr, nullptr, false)) return false;
+    S.tile_cfg = tile_cfg;
     const TileLayout L = tile_layout(P, S, (int)sizeof(T));
     int n = 0;
     for (size_t q = 0; q < P.in_names.size(); ++q) {
@@ -1516,8 +1532,8 @@ static bool tiled_possible(const Program &P, const oec_field *const *in, const i
 }
 
 struct Tuned {
-    int variant;
-    float us[6];
+    int variant, tile_cfg;
+    float us[5 + N_TILE_CFGS];
 };
 static std::map<std::string, Tuned> g_tuned;
 
@@ -1531,18 +1547,28 @@ static oec_status run(const Program &P, const oec_field *const *in, oec_field *c
     const int device = in[0]->device;
     S.variant = -1;  // variant-free key
     const std::string key = spec_key(P, S, device);
-    int tuned = -1;
+    int tuned = -1, tuned_cfg = 0;
     {
         std::lock_guard<std::mutex> g(g_mu);  // released before launching (get_compiled locks it)
         auto it = g_tuned.find(key);
-        if (it != g_tuned.end()) tuned = it->second.variant;
+        if (it != g_tuned.end()) {
+            tuned = it->second.variant;
+            tuned_cfg = it->second.tile_cfg;
+        }
     }
-    if (tuned >= 0) return run_variant<T>(P, in, out, sc, lo, hi, tuned, s);
+    if (tuned >= 0) return run_variant<T>(P, in, out, sc, lo, hi, tuned, s, tuned_cfg);
     cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
     if (cudaStreamIsCapturing(s, &cap) != cudaSuccess || cap != cudaStreamCaptureStatusNone)
         return run_variant<T>(P, in, out, sc, lo, hi, OEC_VARIANT_NAIVE, s);
-    static const int cand[6] = {OEC_VARIANT_NAIVE, OEC_VARIANT_UNROLL2, OEC_VARIANT_UNROLL4, OEC_VARIANT_UNROLL2_K,
-                                OEC_VARIANT_UNROLL4_K, OEC_VARIANT_TILED};
+    // candidates: inline, unroll 2/4 along j and k, and every tiled configuration
+    const int NC = 5 + N_TILE_CFGS;
+    int cand[5 + N_TILE_CFGS], cfg[5 + N_TILE_CFGS];
+    const int fixed[5] = {OEC_VARIANT_NAIVE, OEC_VARIANT_UNROLL2, OEC_VARIANT_UNROLL4, OEC_VARIANT_UNROLL2_K,
+                          OEC_VARIANT_UNROLL4_K};
+    for (int c = 0; c < NC; ++c) {
+        cand[c] = c < 5 ? fixed[c] : OEC_VARIANT_TILED;
+        cfg[c] = c < 5 ? 0 : c - 5;
+    }
     int l2 = 0;
     cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, device);
     const size_t flush_bytes = (size_t)std::max(l2, 1 << 20) * 2;
@@ -1551,20 +1577,20 @@ static oec_status run(const Program &P, const oec_field *const *in, oec_field *c
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
-    Tuned best{OEC_VARIANT_NAIVE, {0, 0, 0, 0, 0, 0}};
+    Tuned best{OEC_VARIANT_NAIVE, 0, {}};
     float best_us = 1e30f;
     int launches = 0;
-    for (int c = 0; c < 6; ++c) {
-        if (cand[c] == OEC_VARIANT_TILED && !tiled_possible<T>(P, in, lo, hi)) {
+    for (int c = 0; c < NC; ++c) {
+        if (cand[c] == OEC_VARIANT_TILED && !tiled_possible<T>(P, in, lo, hi, cfg[c])) {
             best.us[c] = -1.f;  // not describable to TMA: not a candidate
             continue;
         }
-        if ((st = run_variant<T>(P, in, out, sc, lo, hi, cand[c], s))) break;  // compile + warm
+        if ((st = run_variant<T>(P, in, out, sc, lo, hi, cand[c], s, cfg[c]))) break;  // compile + warm
         float tot = 0.f;
         for (int rep = 0; rep < 3 && !st; ++rep) {
             if (flush) cudaMemsetAsync(flush, rep, flush_bytes, s);
             cudaEventRecord(e0, s);
-            st = run_variant<T>(P, in, out, sc, lo, hi, cand[c], s);
+            st = run_variant<T>(P, in, out, sc, lo, hi, cand[c], s, cfg[c]);
             cudaEventRecord(e1, s);
             cudaEventSynchronize(e1);
             float ms = 0.f;
@@ -1576,6 +1602,7 @@ static oec_status run(const Program &P, const oec_field *const *in, oec_field *c
         if (best.us[c] < best_us) {
             best_us = best.us[c];
             best.variant = cand[c];
+            best.tile_cfg = cfg[c];
         }
         launches += 4;
     }
@@ -1613,6 +1640,29 @@ static ProgDesc make_desc(const std::shared_ptr<Registered> &R) {
 }
 
 }  // namespace jit
+
+std::shared_ptr<const ProgDesc> jit_internal(const char *source) {
+    static std::map<const char *, std::shared_ptr<jit::Registered>> cache;  // keyed by the text's address
+    std::lock_guard<std::mutex> g(jit::g_mu);
+    auto it = cache.find(source);
+    if (it == cache.end()) {
+        auto R = std::make_shared<jit::Registered>();
+        try {
+            jit::Parser ps;
+            ps.t = jit::lex(source);
+            ps.parse();
+            R->prog = std::move(ps.P);
+            jit::infer_shapes(R->prog);
+        } catch (const jit::Error &e) {
+            set_error(OEC_ERR_ARG, "internal stencil program: %s", e.msg.c_str());
+            return nullptr;
+        }
+        R->prog.uid = ++jit::g_uid;
+        R->desc = jit::make_desc(R);
+        it = cache.emplace(source, R).first;
+    }
+    return std::shared_ptr<const ProgDesc>(it->second, &it->second->desc);
+}
 
 std::shared_ptr<const ProgDesc> jit_lookup(const char *name) {
     std::lock_guard<std::mutex> g(jit::g_mu);

@@ -151,6 +151,11 @@ struct ProgDesc {
 };
 // JIT registry (csrc/jit.cpp): the program registered under `name`, or null
 std::shared_ptr<const ProgDesc> jit_lookup(const char *name);
+// a program compiled from library-internal text (not visible by name), cached per text; null
+// (with the error set) if it does not parse
+std::shared_ptr<const ProgDesc> jit_internal(const char *source);
+// stencil-language text of a builtin suite program (csrc/programs.cpp), or null
+const char *builtin_program_text(int program_id);
 // true for the hand-written programs of the builtin registry (runtime.cpp)
 bool builtin_program(const char *name);
 

@@ -6,6 +6,7 @@
 // checks them against the oracle's brute-force touched-index trace.
 #include <cuda_runtime.h>
 #include <stdarg.h>
+#include <stdlib.h>
 #include <stdio.h>
 #include <string.h>
 
@@ -391,7 +392,24 @@ static oec_status run_device(int p, const oec_field *const *in, oec_field *const
                             &launches);
         break;
     }
-    default: e = launch_suite<T>(p, v_in, v_out, sc, d, unroll_of(p, variant), s, &launches); break;
+    default: {
+        // AUTO: the library's compiler (csrc/jit.cpp) on the program's stencil-language text
+        // (csrc/programs.cpp), tuned over inline / unrolled / TMA-tiled kernels; the
+        // hand-written kernels serve the explicit variants, and AUTO when NVRTC is unavailable
+        // (OEC_BUILTIN_JIT=0 forces them).
+        static const bool use_jit = !(getenv("OEC_BUILTIN_JIT") && getenv("OEC_BUILTIN_JIT")[0] == '0');
+        if (variant == OEC_VARIANT_AUTO && use_jit) {
+            if (const char *txt = builtin_program_text(p)) {
+                auto J = jit_internal(txt);
+                if (J) {
+                    oec_status st = J->run(sizeof(T) == 4 ? OEC_F32 : OEC_F64, in, out, sc, lo, hi, OEC_VARIANT_AUTO, s);
+                    if (st != OEC_ERR_UNSUPPORTED) return st;  // launches counted by the JIT
+                }
+            }
+        }
+        e = launch_suite<T>(p, v_in, v_out, sc, d, unroll_of(p, variant), s, &launches);
+        break;
+    }
     }
     if (e != cudaSuccess) return set_error(OEC_ERR_CUDA, "%s: kernel launch failed: %s", P.name, cudaGetErrorString(e));
     g_launches = launches;

@@ -224,7 +224,20 @@ def test_auto_tuning_is_cached_and_bit_identical():
     ref = oracle(tp, host, (0, 0, 0), domain)
     got, n1 = run_jit(name, tp, host, domain, 0)
     check(got, ref, (0, 0, 0), domain)
-    assert n1 == 24  # 6 candidates x (1 warm-up + 3 timed)
+    assert n1 == 36  # 9 candidates (5 + 4 tiled configurations) x (1 warm-up + 3 timed)
     got, n2 = run_jit(name, tp, host, domain, 0)
     check(got, ref, (0, 0, 0), domain)
     assert n2 == 1
+
+
+@pytest.mark.parametrize("cfg", [0, 1, 2, 3])
+@pytest.mark.parametrize("program", ["hdiff", "nh_p_grad", "fvtp2d_qj", "fastwaves"])
+def test_tiled_configurations(program, cfg, monkeypatch):
+    """Every tiled configuration AUTO may pick (rows per thread x ring budget), ragged domain."""
+    monkeypatch.setenv("OEC_JIT_TILE_CFG", str(cfg))
+    name = registered(text_of(program))
+    tp = dsl.parse(text_of(program))
+    domain = (200, 70, 9)
+    host = synth.make_inputs(program, domain, seed=cfg)
+    got, _ = run_jit(name, tp, host, domain, 7)
+    check(got, oracle(tp, host, (0, 0, 0), domain), (0, 0, 0), domain)

@@ -220,3 +220,11 @@ def test_k_unroll_shares_levels():
 def test_k_unroll_rejected_for_builtins():
     st, msg = _status(lambda: oec.oec_apply_program("uvbke", [], [], None, (0, 0, 0), (8, 8, 2), oec.OEC_VARIANT_UNROLL2_K))
     assert st in (1, 7)
+
+
+def test_embedded_suite_texts_equal_test_programs():
+    """The library compiles its builtin suite programs' AUTO kernels from embedded stencil-language
+    text (csrc/programs.cpp); it must be the very text the oracle reader is pinned on."""
+    src = open(os.path.join(os.path.dirname(HERE), "paper_2005_13014_b200", "csrc", "programs.cpp")).read()
+    for program in ("uvbke", "p_grad_c", "nh_p_grad", "fvtp2d_qi", "fvtp2d_qj", "fvtp2d_flux", "fastwaves"):
+        assert 'R"OEC(' + text_of(program) + ')OEC"' in src, program

@@ -20,6 +20,7 @@ def main():
     ap.add_argument("--reps", type=int, default=6)
     ap.add_argument("--sets", type=int, default=4)
     ap.add_argument("--variant", type=int, default=0)
+    ap.add_argument("--text", action="store_true", help="run the stencil-language version (tests/programs) via the JIT")
     a = ap.parse_args()
     import torch
 
@@ -34,9 +35,13 @@ def main():
         ins = [oec.field_from_host(host[s.name]) for s in spec.inputs]
         outs = [oec.empty_like_domain(dom, fill=0.0) for _ in spec.outputs]
         sets.append((ins, outs))
+    name = a.program
+    if a.text:
+        with open(os.path.join(ROOT, "tests", "programs", a.program + ".oec")) as f:
+            name = oec.oec_program_create(f.read())
     for r in range(a.reps):
         ins, outs = sets[r % a.sets]
-        oec.oec_apply_program(a.program, ins, outs, sc, (0, 0, 0), dom, a.variant)
+        oec.oec_apply_program(name, ins, outs, sc, (0, 0, 0), dom, a.variant)
     torch.cuda.synchronize()
     print("done", a.program, dom, a.reps)
 
