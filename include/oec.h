@@ -402,6 +402,11 @@ oec_status oec_ipc_close(void *dev_ptr);
 oec_status oec_selftest_rcp(unsigned long long n, unsigned long long seed, unsigned long long *mismatches,
                             unsigned long long *checked);
 
+/* The f32 vadv kernel's branch-free binary32 reciprocal (seed + one fused Newton step) checked
+ * against 1.0f / x on EVERY 32-bit pattern for which it claims to apply (normal x with exponent
+ * field in [2, 252]).  Synchronous. */
+oec_status oec_selftest_rcp32(unsigned long long *mismatches, unsigned long long *checked);
+
 #ifdef __cplusplus
 }
 #endif

@@ -114,6 +114,7 @@ SIGNATURES = {
     "oec_program_generate": (C.c_int, [C.c_char_p, _PP, C.c_int32, _PP, C.c_int32, C.POINTER(C.c_int64),
                                        C.POINTER(C.c_int64), C.c_int32, C.c_int32, C.c_char_p, C.c_int64,
                                        C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+    "oec_selftest_rcp32": (C.c_int, [C.POINTER(C.c_ulonglong), C.POINTER(C.c_ulonglong)]),
     "oec_selftest_rcp": (C.c_int, [C.c_ulonglong, C.c_ulonglong, C.POINTER(C.c_ulonglong), C.POINTER(C.c_ulonglong)]),
 }
 
@@ -461,6 +462,13 @@ def oec_halo_exchange_local(global_domain, px: int, py: int, fields: Sequence[Fi
     arr = (_P * len(fields))(*[f.ptr for f in fields])
     _check(lib().oec_halo_exchange_local(_i64(global_domain), px, py, arr, n_per_rank, _i32(width_lo), _i32(width_hi),
                                          _stream(stream)))
+
+
+def oec_selftest_rcp32():
+    """(mismatches, checked) of the exhaustive binary32 reciprocal self-test (include/oec.h)."""
+    bad, used = C.c_ulonglong(), C.c_ulonglong()
+    _check(lib().oec_selftest_rcp32(C.byref(bad), C.byref(used)))
+    return bad.value, used.value
 
 
 def oec_selftest_rcp(n: int, seed: int = 1):

@@ -77,3 +77,11 @@ def test_f32_host_buffers_end_to_end():
         r = run_oracle(program, host, domain)
         for name, o in zip(spec.outputs, outs_np):
             assert compare(o, r[name])["n_bitdiff"] == 0, (program, name)
+
+
+def test_branch_free_rcp32_is_ieee_exhaustive():
+    """The f32 vadv reciprocal equals 1.0f / x bit for bit on every float where it applies."""
+    from paper_2005_13014_b200 import oec
+
+    bad, used = oec.oec_selftest_rcp32()
+    assert used > 3_000_000_000 and bad == 0, (bad, used)
