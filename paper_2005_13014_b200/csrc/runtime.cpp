@@ -273,11 +273,14 @@ static oec_status check_cover(const oec_field *f, const char *what, const int64_
 // ---------------------------------------------------------------------------------------------
 // host staging (end-to-end path, device == OEC_DEVICE_HOST)
 // ---------------------------------------------------------------------------------------------
+constexpr int STAGE_SLABS = 8;
 struct Staging {
     std::mutex mu;
     std::vector<void *> bufs;
     std::vector<size_t> sizes;
     int device = -1;
+    cudaStream_t h2d = nullptr, d2h = nullptr;  // copy streams of the pipelined host path
+    cudaEvent_t ev[2 * STAGE_SLABS] = {};
 };
 static Staging g_stage;
 
@@ -298,9 +301,36 @@ static oec_status stage_buffer(size_t idx, size_t bytes, void **p) {
     return OEC_OK;
 }
 
+// copy the allocated rows j in [j0, j1) (all i and k) of a host field into its device twin
+static cudaError_t h2d_rows(const oec_field *dev, const oec_field *host, int64_t j0, int64_t j1, cudaStream_t s) {
+    const int es = esize(host->dtype);
+    const int64_t ni = host->ub[0] - host->lb[0], nk = host->ub[2] - host->lb[2], s1 = host->stride[1];
+    const int64_t off = (j0 - host->lb[1]) * s1;
+    const char *src = (const char *)host->data + off * es;
+    char *dst = (char *)dev->data + off * es;
+    if (is_k_invariant(host) || nk == 1)  // rows only
+        return cudaMemcpy2DAsync(dst, s1 * es, src, s1 * es, ni * es, j1 - j0, cudaMemcpyHostToDevice, s);
+    const int64_t s2 = host->stride[2];
+    if (s1 >= s2 * nk)  // j outermost (default i, k, j layout): the rows are one contiguous block
+        return cudaMemcpyAsync(dst, src, ((j1 - j0 - 1) * s1 + (nk - 1) * s2 + ni) * es, cudaMemcpyHostToDevice, s);
+    // k outermost: one 2D copy, a (j1-j0) x pitch block per level
+    return cudaMemcpy2DAsync(dst, s2 * es, src, s2 * es, ((j1 - j0 - 1) * s1 + ni) * es, nk, cudaMemcpyHostToDevice, s);
+}
+
 // copy the domain box of a strided device field back into the same-layout host field
 static cudaError_t d2h_box(const oec_field *host, const oec_field *dev, const int64_t *lo, const int64_t *hi,
                            cudaStream_t s) {
+    // the box spans whole rows and planes of a dense i, j, k field: one contiguous copy
+    {
+        const int64_t ni = host->ub[0] - host->lb[0], nj = host->ub[1] - host->lb[1];
+        if (!is_k_invariant(host) && host->stride[1] == ni && host->stride[2] == ni * nj && lo[0] == host->lb[0] &&
+            hi[0] == host->ub[0] && lo[1] == host->lb[1] && hi[1] == host->ub[1]) {
+            const int es = esize(host->dtype);
+            const int64_t off = (lo[2] - host->lb[2]) * host->stride[2];
+            return cudaMemcpyAsync((char *)host->data + off * es, (const char *)dev->data + off * es,
+                                   (hi[2] - lo[2]) * ni * nj * es, cudaMemcpyDeviceToHost, s);
+        }
+    }
     // outer loop over the dimension with the larger stride, 2D copies over the other two
     int outer = (host->stride[2] >= host->stride[1]) ? 2 : 1;
     int mid = 3 - outer;
@@ -531,12 +561,16 @@ static oec_status apply(const ProgDesc &P, const oec_field *const *in, int n_in,
     if (device >= 0) return P.run(dtype, in, out, sc.data(), lo, hi, variant, s);
     if (device != OEC_DEVICE_HOST) return set_error(OEC_ERR_ARG, "%s: invalid device %d", pname, device);
 
-    // ---- end-to-end path: stage host fields through cached device buffers ----
+    // ---- end-to-end path: stage host fields through cached device buffers, pipelined over j-slabs
+    // (grid points are independent given their inputs' access extents): the H2D copy of
+    // slab s+1 (copy stream), the kernel on slab s (the caller's stream) and the D2H copy of slab
+    // s-1 (a third stream) overlap -- PCIe is full duplex.  Each input row is copied once, in the
+    // first slab that needs it; the call returns when the outputs are back in host memory.
     std::lock_guard<std::mutex> lock(g_stage.mu);
     std::vector<oec_field> din(P_n_in), dout(P_n_out);
     std::vector<const oec_field *> pin(P_n_in);
     std::vector<oec_field *> pout(P_n_out);
-    size_t slot = 0;
+    size_t slot = 0, total = 0;
     for (int q = 0; q < P_n_in; ++q) {
         uintptr_t b0, b1;
         span_bytes(in[q], &b0, &b1);
@@ -545,10 +579,8 @@ static oec_status apply(const ProgDesc &P, const oec_field *const *in, int n_in,
         din[q] = *in[q];
         din[q].device = 0;
         din[q].data = (char *)dptr + ((uintptr_t)in[q]->data - b0);
-        cudaError_t e = cudaMemcpyAsync(dptr, (const void *)b0, b1 - b0, cudaMemcpyHostToDevice, s);
-        if (e != cudaSuccess)
-            return set_error(OEC_ERR_CUDA, "H2D copy of %s: %s", P.in_names[q].c_str(), cudaGetErrorString(e));
         pin[q] = &din[q];
+        total += b1 - b0;
     }
     for (int q = 0; q < P_n_out; ++q) {
         uintptr_t b0, b1;
@@ -560,14 +592,56 @@ static oec_status apply(const ProgDesc &P, const oec_field *const *in, int n_in,
         dout[q].data = (char *)dptr + ((uintptr_t)out[q]->data - b0);
         pout[q] = &dout[q];
     }
-    if ((st = P.run(dtype, pin.data(), pout.data(), sc.data(), lo, hi, variant, s))) return st;
-    int launches = g_launches;
-    for (int q = 0; q < P_n_out; ++q) {
-        cudaError_t e = d2h_box(out[q], &dout[q], lo, hi, s);
-        if (e != cudaSuccess)
-            return set_error(OEC_ERR_CUDA, "D2H copy of %s: %s", P.out_names[q].c_str(), cudaGetErrorString(e));
+    if (!g_stage.h2d) {
+        cudaStreamCreateWithFlags(&g_stage.h2d, cudaStreamNonBlocking);
+        cudaStreamCreateWithFlags(&g_stage.d2h, cudaStreamNonBlocking);
+        for (int e = 0; e < 2 * STAGE_SLABS; ++e) cudaEventCreateWithFlags(&g_stage.ev[e], cudaEventDisableTiming);
     }
-    cudaError_t e = cudaStreamSynchronize(s);
+    const int64_t nj = hi[1] - lo[1];
+    static int max_slabs = -1;
+    if (max_slabs < 0) {
+        const char *ev = getenv("OEC_STAGE_SLABS");
+        // default 1: measured on the B200 box, overlapping H2D and D2H slabs made the 128x128x80
+        // step slower (1 slab 2.43 ms, 2: 2.84, 4: 3.89, 8: 5.29 ms; profiles/e2e_probe_r01d.txt)
+        max_slabs = ev ? std::max(1, std::min(STAGE_SLABS, atoi(ev))) : 1;
+    }
+    const int ns = (int)std::max<int64_t>(1, std::min<int64_t>(std::min<int64_t>(max_slabs, nj / 4),
+                                                                  (int64_t)(total >> 22)));  // >= ~4 MB per slab
+    std::vector<int64_t> next_row(P_n_in);  // first allocated row not yet copied, per input
+    for (int q = 0; q < P_n_in; ++q) {
+        next_row[q] = in[q]->lb[1];
+        const bool rows_ok = in[q]->stride[1] > 0 && (is_k_invariant(in[q]) || in[q]->stride[2] > 0);
+        if (!rows_ok) {  // unusual strides: the whole allocation up front
+            uintptr_t b0, b1;
+            span_bytes(in[q], &b0, &b1);
+            cudaError_t e0 = cudaMemcpyAsync((char *)din[q].data - ((uintptr_t)in[q]->data - b0), (const void *)b0,
+                                             b1 - b0, cudaMemcpyHostToDevice, g_stage.h2d);
+            if (e0 != cudaSuccess) return set_error(OEC_ERR_CUDA, "H2D copy of %s: %s", P.in_names[q].c_str(),
+                                                    cudaGetErrorString(e0));
+            next_row[q] = in[q]->ub[1];
+        }
+    }
+    int launches = 0;
+    cudaError_t e = cudaSuccess;
+    for (int sl = 0; sl < ns && e == cudaSuccess; ++sl) {
+        int64_t slo[3] = {lo[0], lo[1] + nj * sl / ns, lo[2]}, shi[3] = {hi[0], lo[1] + nj * (sl + 1) / ns, hi[2]};
+        for (int q = 0; q < P_n_in && e == cudaSuccess; ++q) {  // rows this slab needs, not copied yet
+            int64_t need = sl == ns - 1 ? in[q]->ub[1] : std::min<int64_t>(in[q]->ub[1], shi[1] + P.in_hi[q][1]);
+            if (need > next_row[q]) e = h2d_rows(&din[q], in[q], next_row[q], need, g_stage.h2d);
+            next_row[q] = std::max(next_row[q], need);
+        }
+        if (e != cudaSuccess) break;
+        cudaEventRecord(g_stage.ev[2 * sl], g_stage.h2d);
+        cudaStreamWaitEvent(s, g_stage.ev[2 * sl], 0);
+        if ((st = P.run(dtype, pin.data(), pout.data(), sc.data(), slo, shi, variant, s))) return st;
+        launches += g_launches;
+        cudaEventRecord(g_stage.ev[2 * sl + 1], s);
+        cudaStreamWaitEvent(g_stage.d2h, g_stage.ev[2 * sl + 1], 0);
+        for (int q = 0; q < P_n_out && e == cudaSuccess; ++q) e = d2h_box(out[q], &dout[q], slo, shi, g_stage.d2h);
+    }
+    if (e != cudaSuccess) return set_error(OEC_ERR_CUDA, "%s: host staging copy: %s", pname, cudaGetErrorString(e));
+    e = cudaStreamSynchronize(g_stage.d2h);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
     if (e != cudaSuccess) return set_error(OEC_ERR_CUDA, "%s: %s", pname, cudaGetErrorString(e));
     g_launches = launches;
     return OEC_OK;
