@@ -17,6 +17,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--domain", type=int, nargs=3, default=[128, 128, 80])
     ap.add_argument("--variant", type=int, default=7)
+    ap.add_argument("--programs", nargs="*", default=None)
     a = ap.parse_args()
     import torch
 
@@ -27,10 +28,12 @@ def main():
     peak, _ = hbm_peak()
     pdir = os.path.join(ROOT, "tests", "programs")
     for fn in sorted(os.listdir(pdir)):
+        if a.programs and fn[:-4] not in a.programs:
+            continue
         with open(os.path.join(pdir, fn)) as f:
             name = oec.oec_program_create(f.read())
         r = program_measure(oec, torch, fn[:-4], dom, l2, peak, a.variant, run_name=name)
-        print(json.dumps({"tile": os.environ.get("OEC_JIT_TILE", "2,110"), "program": fn[:-4], "domain": list(dom),
+        print(json.dumps({"tile_cfg": os.environ.get("OEC_JIT_TILE_CFG", "0"), "variant": a.variant, "program": fn[:-4], "domain": list(dom),
                           "us": round(r["us_per_launch"], 2), "frac": round(r["frac_of_hbm_peak"], 3)}), flush=True)
         oec.oec_program_destroy(name)
 
