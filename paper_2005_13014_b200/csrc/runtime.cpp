@@ -656,9 +656,10 @@ extern "C" {
 int32_t oec_abi_version(void) { return OEC_ABI_VERSION; }
 
 const char *oec_build_info(void) {
-    return "liboec: sm_100a, fp64 + f32, --fmad=false; kernels: hdiff (TMA ring, rolling-j, naive/unrolled, unfused), "
-           "vadv (TMEM c'/d' specialised, TMA smem, one thread per column, unfused), suite (inlined per point, "
-           "unrolled along j, unfused per operator), halo (pack/unpack, NCCL send/recv)";
+    return "liboec: sm_100a, fp64 + f32, --fmad=false; kernels: hdiff (TMA ring, rolling-j, naive/unrolled, unfused, "
+           "fused-exchange pipeline), vadv (TMEM c'/d' f64+f32, TMA smem, one thread per column, unfused), suite "
+           "(stencil-language JIT: inline/unrolled/TMA-tiled, tuned; hand-written inlined/unrolled/unfused), halo "
+           "(pack/unpack, NCCL send/recv)";
 }
 
 const char *oec_last_error(void) { return g_err; }
