@@ -651,6 +651,8 @@ struct TileLayout {
 // tiled configurations (rows per thread, shared-memory budget per CTA in KB): fewer rows and a
 // smaller ring give more resident CTAs (latency hiding), more rows share loads between rows;
 // AUTO tries them all, OEC_VARIANT_TILED uses the first (measured best on most of the suite).
+// (measured: deeper rings -- {1, 110}, {1, 80} -- are slower at 128^2 and 1024^2; more resident
+// CTAs matter more than bytes in flight per CTA, profiles/ncu_summary_r01.md)
 static const int TILE_CFGS[][2] = {{1, 56}, {1, 36}, {2, 110}, {4, 110}};
 static const int N_TILE_CFGS = 4;
 
