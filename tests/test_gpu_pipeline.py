@@ -175,7 +175,7 @@ def test_pipeline_errors():
 
 def test_ipc_export_roundtrip_offsets():
     """oec_ipc_export reports the byte offset of an interior pointer in its allocation (the
-    import side needs another process; the bench's multi-GPU peer path exercises it)."""
+    import side needs another process: tests/test_gpu_pipeline_ipc.py)."""
     from paper_2005_13014_b200 import oec
 
     f = oec.oec_field_create((64, 8, 2), (0, 0, 0), (0, 0, 0))
