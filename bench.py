@@ -434,12 +434,13 @@ def main():
         e2e = e2e_measure(oec, torch, hh, vh, dtr, domain, args.e2e_steps, world)
 
     # ---- remaining suite (evidence for SURVEY §8(a) a7; not part of the step) ----
-    suite_res = levels = f32_res = jit_res = None
+    suite_res = levels = f32_res = jit_res = pipe_res = None
     if not args.no_suite and world == 1:
         suite_res = suite_measure(oec, torch, domain, l2, peak)
         levels = levels_measure(oec, torch, domain, l2, peak)
         f32_res = f32_measure(oec, torch, domain, l2, peak)
         jit_res = jit_measure(oec, torch, domain, l2, peak)
+        pipe_res = pipeline_measure(oec, torch, domain, l2, peak)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -473,6 +474,8 @@ def main():
             res["f32"] = f32_res
         if jit_res is not None:
             res["jit"] = jit_res
+        if pipe_res is not None:
+            res["hdiff_pipeline"] = pipe_res
         print(json.dumps(res), flush=True)
     if decomp:
         dist.barrier()
@@ -591,6 +594,43 @@ def jit_measure(oec, torch, domain, l2, peak):
             oec.oec_program_destroy(name)
         res[program] = r
     return res
+
+
+def pipeline_measure(oec, torch, domain, l2, peak, reps=20):
+    """The fused-exchange multi-step hdiff (oec_hdiff_pipeline) on one rank
+    (px = py = 1: no neighbours, every tile interior): us per step next to hdiff's algorithmic bytes.
+    R independent pipelines (each its own x0 / x1 / coeff) are stepped round-robin so the fields
+    stream from HBM (R sets > 4x L2).  Cross-process correctness: tests/test_gpu_pipeline_ipc.py."""
+    host = synth.make_inputs("hdiff", domain, seed=0)
+    per = 3 * (domain[0] + 4) * (domain[1] + 4) * domain[2] * 8
+    R = max(2, math.ceil(4 * l2 / per) + 1)
+    pipes = []
+    for _ in range(R):
+        x0 = oec.field_from_host(host["in"])
+        x1 = oec.field_from_host(host["in"])
+        cf = oec.field_from_host(host["coeff"])
+        pipes.append(oec.HdiffPipeline(domain, 1, 1, 0, cf, x0, x1))
+    for p in pipes:
+        p.run(1)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for p in pipes:
+            p.run(1)
+    g.replay()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(reps):
+        g.replay()
+    b.record()
+    torch.cuda.synchronize()
+    us = 1e3 * a.elapsed_time(b) / (reps * R)
+    nbytes = hdiff_bytes(*domain)
+    del pipes, g
+    return {"us_per_step": us, "algorithmic_bytes": nbytes, "GB/s": nbytes / (us * 1e-6) / 1e9,
+            "frac_of_hbm_peak": nbytes / (us * 1e-6) / 1e9 / peak, "pipelines": R,
+            "note": "one rank (no neighbours); steps of R independent pipelines round-robin, fields > 4x L2"}
 
 
 def levels_measure(oec, torch, domain, l2, peak):

@@ -666,6 +666,15 @@ __global__ void __launch_bounds__(NW * 32, 1) hdiff_pipe(const __grid_constant__
     unsigned char *wbase = smem + warp * S * C::SLOT;
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem + NW * S * C::SLOT) + warp * S;
     const int gw = blockIdx.x * NW + warp, nwt = gridDim.x * NW;
+    // programmatic dependent launch: descriptor prefetch overlaps the previous step's drain; the
+    // step counter and x_t are read only after the previous grid completed
+    if (lane == 0) {
+        prefetch_tmap(&m0.map);
+        prefetch_tmap(&m1.map);
+        prefetch_tmap(&m_cf.map);
+    }
+    griddep_launch_dependents();
+    griddep_wait();
     const unsigned long long t = *reinterpret_cast<volatile const unsigned long long *>(a.pad + PIPE_PAD_STEP);
     const int b = (int)(t & 1);
     const TMap &m_in = b ? m1 : m0;
@@ -689,8 +698,6 @@ __global__ void __launch_bounds__(NW * 32, 1) hdiff_pipe(const __grid_constant__
     };
 
     if (lane == 0) {
-        prefetch_tmap(&m_in.map);
-        prefetch_tmap(&m_cf.map);
 #pragma unroll
         for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
         fence_mbar_init();
@@ -784,10 +791,12 @@ __global__ void __launch_bounds__(NW * 32, 1) hdiff_pipe(const __grid_constant__
         __syncwarp();
     }
     (void)nk;
-    // ---- publish "step t done" (our outputs written, our reads of the neighbours' x_t finished)
-    __threadfence_system();
+    // ---- publish "step t done" (our outputs written, our reads of the neighbours' x_t finished):
+    // every thread's accesses precede the barrier; thread 0's system-scope fence (cumulative)
+    // then orders them before the CTA is counted as done
     __syncthreads();
     if (threadIdx.x == 0) {
+        __threadfence_system();
         const unsigned long long old = atomicAdd(a.pad + PIPE_PAD_FINISHED, 1ull);
         if (old == gridDim.x - 1) {
             a.pad[PIPE_PAD_FINISHED] = 0;
@@ -817,9 +826,10 @@ cudaError_t launch_pipe(const TMap &m0, const TMap &m1, const TMap &mcf, const P
     }
     const long long blocks = std::max(1ll, std::min<long long>((a.n_items + NW - 1) / NW, (long long)sms * blocks_per_sm));
     for (int s = 0; s < nsteps; ++s) {
-        hdiff_pipe<T, V, JB, S, NW><<<(unsigned)blocks, NW * 32, C::SMEM, st>>>(m0, m1, mcf, a);
+        cudaError_t e = launch_pdl(hdiff_pipe<T, V, JB, S, NW>, dim3((unsigned)blocks), dim3(NW * 32), C::SMEM, st, m0,
+                                   m1, mcf, a);
         ++*launches;
-        cudaError_t e = cudaGetLastError();
+        if (e == cudaSuccess) e = cudaGetLastError();
         if (e != cudaSuccess) return e;
     }
     return cudaSuccess;
