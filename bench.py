@@ -242,6 +242,36 @@ class StepSet:
         return sum(int(np.prod([f.ub[d] - f.lb[d] for d in range(3)])) * 8 for f in fs)
 
 
+def fused_pipelines(oec, dist, sets, domain, world, rank, dev_index):
+    """N > 1, --exchange fused: one oec_hdiff_pipeline per rotating set over this rank's j-slab of
+    the global 128 x 128N x 80 domain (x0 = the set's hdiff input with its halo, x1 a copy: the
+    global outer halo stays constant); fields and signal pads are exported with CUDA IPC, the
+    handles all-gathered, and every pipeline registers its j-neighbours' (imported) fields."""
+    gdom = (domain[0], domain[1] * world, domain[2])
+    mine = []
+    for s in sets:
+        x1 = oec.oec_field_create(domain, (2, 2, 0), (2, 2, 0))
+        x1.view().copy_(s.h_in.view())
+        s.x1 = x1
+        s.pipe = oec.HdiffPipeline(gdom, 1, world, rank, s.h_cf, s.h_in, x1)
+        pad, _ = s.pipe.signal_pad()
+        mine.append(dict(x0=oec.oec_ipc_export(s.h_in.desc.data), x1=oec.oec_ipc_export(x1.desc.data),
+                         pad=oec.oec_ipc_export(pad), desc=oec.field_descriptor(s.h_in)))
+    import torch
+
+    torch.cuda.synchronize()
+    everyone = [None] * world
+    dist.all_gather_object(everyone, mine)
+    for q in (rank - 1, rank + 1):
+        if not 0 <= q < world:
+            continue
+        for si, s in enumerate(sets):
+            Q = everyone[q][si]
+            p0, p1, pp = (oec.oec_ipc_import(*Q[k]) for k in ("x0", "x1", "pad"))
+            s.pipe.set_peer(q, oec.field_at(p0, Q["desc"], dev_index), oec.field_at(p1, Q["desc"], dev_index), pp)
+    dist.barrier()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -255,6 +285,13 @@ def main():
     ap.add_argument("--sets", type=int, default=0, help="rotating input sets (0 = auto, > 4x L2)")
     ap.add_argument("--force-decomp", action="store_true",
                     help="debug: run the N>1 code path (NCCL process group, decomposition, exchange) even at N=1")
+    ap.add_argument("--exchange", default="fused", choices=["fused", "nccl"],
+                    help="N>1 halo exchange of hdiff: 'fused' = oec_hdiff_pipeline (each step one kernel that "
+                         "reads the neighbours' halo cells from their memory over NVLink, CUDA IPC), 'nccl' = "
+                         "oec_halo_exchange (NCCL send/recv on a comm stream, concurrent with vadv)")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="process-group backend (gloo: testing the fused path with all ranks on one GPU, "
+                         "OEC_BENCH_DEVICE=0)")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -269,16 +306,23 @@ def main():
     from paper_2005_13014_b200 import oec
 
     oec.lib()  # fail loudly if the extension is missing
-    torch.cuda.set_device(local_rank)
+    dev_index = int(os.environ.get("OEC_BENCH_DEVICE", local_rank))
+    torch.cuda.set_device(dev_index)
     dev = torch.cuda.current_device()
     decomp = world > 1 or args.force_decomp
+    fused = decomp and args.exchange == "fused"
+    if args.dist_backend == "gloo" and not fused:
+        raise SystemExit("--dist-backend gloo needs --exchange fused")
     if decomp:
         if world == 1:
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
             os.environ.setdefault("MASTER_PORT", "29517")
             os.environ.setdefault("RANK", "0")
             os.environ.setdefault("WORLD_SIZE", "1")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev_index))
+        else:
+            dist.init_process_group("gloo")
     props = torch.cuda.get_device_properties(dev)
     l2 = int(getattr(props, "L2_cache_size", 126 * 2**20))
     domain = DOMAIN
@@ -286,11 +330,9 @@ def main():
 
     # ---- decomposition (N > 1): j-slabs of the global 128 x 128N x 80 domain ----
     dec = None
-    if decomp:
-        from torch._C._distributed_c10d import ProcessGroupNCCL
-
+    if decomp and not fused:
         pg = dist.distributed_c10d._get_default_group()
-        nccl_pg = pg._get_backend(torch.device("cuda", local_rank))
+        nccl_pg = pg._get_backend(torch.device("cuda", dev_index))
         dist.barrier()
         nccl_comm = nccl_pg._comm_ptr()
         dec = oec.oec_decomp_create((domain[0], domain[1] * world, domain[2]), 1, world, rank, nccl_comm)
@@ -302,11 +344,31 @@ def main():
     first = StepSet(oec, hh, vh, domain)
     R = args.sets or max(2, math.ceil(4 * l2 / first.nbytes()) + 1)
     sets = [first] + [StepSet(oec, hh, vh, domain) for _ in range(R - 1)]
+    fused_note = None
+    if fused:
+        try:
+            fused_pipelines(oec, dist, sets, domain, world, rank, dev_index)
+            ok = 1
+        except Exception as e:  # e.g. no peer access: every rank falls back to the NCCL exchange
+            ok, fused_note = 0, f"fused pipeline unavailable ({type(e).__name__}: {e}); NCCL exchange used"
+        flag = torch.tensor([ok], dtype=torch.int32, device="cuda" if args.dist_backend == "nccl" else "cpu")
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        if int(flag.item()) == 0:
+            if args.dist_backend != "nccl":
+                raise SystemExit(fused_note or "fused pipeline failed on another rank")
+            fused = False
+            fused_note = fused_note or "fused pipeline failed on another rank; NCCL exchange used"
+            pg = dist.distributed_c10d._get_default_group()
+            dec = oec.oec_decomp_create((domain[0], domain[1] * world, domain[2]), 1, world, rank,
+                                        pg._get_backend(torch.device("cuda", dev_index))._comm_ptr())
 
     launches = {"hdiff": 0, "vadv": 0, "halo": 0}
 
     def hdiff(s):
-        oec.oec_hdiff(s.h_in, s.h_cf, s.h_out, (0, 0, 0), domain)
+        if fused:  # one step of this set's pipeline: hdiff with the halo read from the neighbours
+            s.pipe.run(1)
+        else:
+            oec.oec_hdiff(s.h_in, s.h_cf, s.h_out, (0, 0, 0), domain)
         launches["hdiff"] = oec.oec_last_launch_count()
 
     def vadv(s):
@@ -406,7 +468,8 @@ def main():
     t_v = sum(e[0].elapsed_time(e[1]) for e in ev)  # vadv (|| halo exchange when N > 1)
     t_h = sum(e[1].elapsed_time(e[2]) for e in ev)
     if world > 1:
-        t = torch.tensor([elapsed_ms, t_h, t_v], device="cuda", dtype=torch.float64)
+        t = torch.tensor([elapsed_ms, t_h, t_v], device="cuda" if args.dist_backend == "nccl" else "cpu",
+                         dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         elapsed_ms, t_h, t_v = [float(x) for x in t.tolist()]
     clk = clocks.result()
@@ -454,11 +517,14 @@ def main():
             "data": "synthetic (seeded numpy PCG64, SURVEY §8(d) distributions)",
             "config": {"workload": WORKLOAD, "domain_per_gpu": list(domain),
                        "global_domain": [domain[0], domain[1] * world, domain[2]],
-                       "parallelism": f"j-slab decomposition 1x{world}, NCCL halo exchange" if world > 1 else "single GPU",
+                       "parallelism": (f"j-slab decomposition 1x{world}, " + (
+                           "hdiff halo read from the neighbours' memory inside the kernel (fused pipeline, CUDA IPC)"
+                           if fused else "NCCL halo exchange")) if world > 1 else "single GPU",
                        "l2": f"inputs larger than L2: {R} rotating input sets, "
                              f"{R * first.nbytes() / 2**20:.0f} MiB total vs {l2 / 2**20:.0f} MiB L2",
                        "timing": "CUDA events on the launching stream around CUDA graphs of R launches per "
-                                 "kernel; max over ranks" + (f"; halo exchange: {x_mode}" if has_x else "")},
+                                 "kernel; max over ranks" + (f"; halo exchange: {x_mode}" if has_x else "")
+                                 + (f"; {fused_note}" if fused_note else "")},
             "roofline": roofline,
             "kernels": kern,
             "cpu_baseline": cpu,
