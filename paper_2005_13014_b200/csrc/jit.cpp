@@ -676,8 +676,8 @@ static TileLayout tile_layout(const Program &P, const Spec &S, int esz) {
     L.ssk.assign(nin, 0);
     int at = 0;
     for (int q = 0; q < nin; ++q) {
-        if (!P.in_used[q] || P.in_kinv[q]) continue;
-        L.staged[q] = 1;
+        if (!P.in_used[q]) continue;
+        L.staged[q] = 1;  // k-invariant inputs: a 2D (i, j) box, read at every level
         int w = L.ti + P.in_hi[q][0] - P.in_lo[q][0];
         // the box starts on a 16-byte boundary (a misaligned start faults with an illegal
         // instruction, measured on B200): up to 16/esz - 1 extra leading columns, whose count (the
@@ -686,9 +686,12 @@ static TileLayout tile_layout(const Program &P, const Spec &S, int esz) {
         w = (w + per16 - 1 + per16 - 1) / per16 * per16;
         L.w[q] = w;
         L.h[q] = L.tj + P.in_hi[q][1] - P.in_lo[q][1];
-        L.dpt[q] = 1 + P.in_hi[q][2] - P.in_lo[q][2];
-        L.swap[q] = S.in_sk[q] < S.in_sj[q];
-        if (L.swap[q]) {  // shared memory [j][k][i]
+        L.dpt[q] = P.in_kinv[q] ? 1 : 1 + P.in_hi[q][2] - P.in_lo[q][2];
+        L.swap[q] = !P.in_kinv[q] && S.in_sk[q] < S.in_sj[q];
+        if (P.in_kinv[q]) {  // shared memory [j][i]; k offsets of a k-invariant input read the same box
+            L.ssj[q] = w;
+            L.ssk[q] = 0;
+        } else if (L.swap[q]) {  // shared memory [j][k][i]
             L.ssk[q] = w;
             L.ssj[q] = w * L.dpt[q];
         } else {  // [k][j][i]
@@ -1160,6 +1163,9 @@ __device__ __forceinline__ void mb_expect(unsigned long long *b, unsigned n) {
 __device__ __forceinline__ void mb_wait(unsigned long long *b, unsigned ph) {
     asm volatile("{\n.reg .pred p;\nW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n@!p bra W_%=;\n}\n"
                  ::"r"(su32(b)), "r"(ph) : "memory"); }
+__device__ __forceinline__ void tma2(void *dst, const TM *m, unsigned long long *b, int c0, int c1) {
+    asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];"
+                 ::"r"(su32(dst)), "l"((unsigned long long)m), "r"(su32(b)), "r"(c0), "r"(c1) : "memory"); }
 __device__ __forceinline__ void tma3(void *dst, const TM *m, unsigned long long *b, int c0, int c1, int c2) {
     asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];"
                  ::"r"(su32(dst)), "l"((unsigned long long)m), "r"(su32(b)), "r"(c0), "r"(c1), "r"(c2) : "memory"); }
@@ -1203,9 +1209,13 @@ static std::string gen_tiled(const Program &P, const Spec &S) {
         for (size_t q = 0; q < P.in_names.size(); ++q) {
             if (!L.staged[q]) continue;
             const std::string cq = "c" + std::to_string(q);
-            w << ind << "    tma3(smem + st_ * " << L.stage_bytes << " + " << L.off[q] << ", &tm" << q << ", &full[st_], "
-              << cq << "x + i0_, " << (L.swap[q] ? cq + "z + k_, " + cq + "y + j0_" : cq + "y + j0_, " + cq + "z + k_")
-              << ");\n";
+            if (P.in_kinv[q])
+                w << ind << "    tma2(smem + st_ * " << L.stage_bytes << " + " << L.off[q] << ", &tm" << q << ", &full[st_], "
+                  << cq << "x + i0_, " << cq << "y + j0_);\n";
+            else
+                w << ind << "    tma3(smem + st_ * " << L.stage_bytes << " + " << L.off[q] << ", &tm" << q << ", &full[st_], "
+                  << cq << "x + i0_, " << (L.swap[q] ? cq + "z + k_, " + cq + "y + j0_" : cq + "y + j0_, " + cq + "z + k_")
+                  << ");\n";
         }
         w << ind << "}\n";
         return w.str();
@@ -1411,7 +1421,7 @@ static oec_status run_variant(const Program &P, const oec_field *const *in, oec_
                 continue;
             }
             const int box[3] = {L.w[q], L.h[q], L.dpt[q]};
-            if (!make_tmap(in[q], box, &tm[q]))
+            if (!(P.in_kinv[q] ? make_tmap2d(in[q], box, &tm[q]) : make_tmap(in[q], box, &tm[q])))
                 return set_error(OEC_ERR_LAYOUT, "%s: input %s cannot be described to TMA (OEC_VARIANT_TILED needs "
                                  "16-byte aligned rows and strides, e.g. oec_field_create)", P.name.c_str(),
                                  P.in_names[q].c_str());
@@ -1419,7 +1429,7 @@ static oec_status run_variant(const Program &P, const oec_field *const *in, oec_
             const int cxa = cx >= 0 ? cx / per16 * per16 : -((-cx + per16 - 1) / per16) * per16;  // round down
             cb[q][0] = cxa;
             cb[q][1] = (int)(lo[1] + P.in_lo[q][1]) - tm[q].lb1;
-            cb[q][2] = (int)(lo[2] + P.in_lo[q][2]) - tm[q].lb2;
+            cb[q][2] = P.in_kinv[q] ? 0 : (int)(lo[2] + P.in_lo[q][2]) - tm[q].lb2;
             cb[q][3] = cx - cxa;  // leading columns before the box's first needed column
             args.push_back((void *)&tm[q].map);
             args.push_back((void *)&cb[q][0]);
@@ -1528,7 +1538,7 @@ static bool tiled_possible(const Program &P, const oec_field *const *in, const i
         ++n;
         TMap tm;
         const int box[3] = {L.w[q], L.h[q], L.dpt[q]};
-        if (!make_tmap(in[q], box, &tm)) return false;
+        if (!(P.in_kinv[q] ? make_tmap2d(in[q], box, &tm) : make_tmap(in[q], box, &tm))) return false;
     }
     return n > 0 && L.smem <= 227 * 1024;
 }

@@ -59,4 +59,33 @@ bool make_tmap(const oec_field *f, const int box[3], TMap *out) {
     return true;
 }
 
+// 2D (i, j) tensor map over a k-invariant field (stride[2] == 0), box {box[0], box[1]}; the
+// third coordinate of the 3D interface is absent.  Same alignment rules as make_tmap.
+bool make_tmap2d(const oec_field *f, const int box[2], TMap *out) {
+    std::call_once(g_once, load_encode);
+    if (!g_encode || !f || f->stride[0] != 1 || f->stride[2] != 0) return false;
+    const int esz = f->dtype == OEC_F32 ? 4 : 8;
+    const int64_t sj = f->stride[1];
+    if (sj <= 0 || (sj * esz % 16)) return false;
+    const uintptr_t data = (uintptr_t)f->data;
+    const uintptr_t base = data & ~(uintptr_t)15;
+    const int ioff = (int)((data - base) / esz);
+    cuuint64_t dims[2] = {(cuuint64_t)(f->ub[0] - f->lb[0] + ioff), (cuuint64_t)(f->ub[1] - f->lb[1])};
+    cuuint64_t strides[1] = {(cuuint64_t)(sj * esz)};
+    cuuint32_t bx[2] = {(cuuint32_t)box[0], (cuuint32_t)box[1]};
+    cuuint32_t es[2] = {1, 1};
+    if (bx[0] * esz % 16 || bx[0] > 256 || bx[1] > 256) return false;
+    memset(out, 0, sizeof *out);
+    CUresult r = g_encode(&out->map, esz == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2,
+                          (void *)base, dims, strides, bx, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return false;
+    out->ioff = ioff;
+    out->lb0 = (int32_t)f->lb[0];
+    out->lb1 = (int32_t)f->lb[1];
+    out->lb2 = 0;
+    out->kj_swap = 0;
+    return true;
+}
+
 }  // namespace oec
