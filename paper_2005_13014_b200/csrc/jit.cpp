@@ -1570,8 +1570,21 @@ static oec_status run(const Program &P, const oec_field *const *in, oec_field *c
     }
     if (tuned >= 0) return run_variant<T>(P, in, out, sc, lo, hi, tuned, s, tuned_cfg);
     cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-    if (cudaStreamIsCapturing(s, &cap) != cudaSuccess || cap != cudaStreamCaptureStatusNone)
-        return run_variant<T>(P, in, out, sc, lo, hi, OEC_VARIANT_NAIVE, s);
+    if (cudaStreamIsCapturing(s, &cap) != cudaSuccess || cap != cudaStreamCaptureStatusNone) {
+        // no tuning (it synchronises) and no compilation (module loading) inside a capture: the
+        // inline kernel if it is already compiled, else OEC_ERR_UNSUPPORTED (builtin programs then
+        // use their hand-written kernels)
+        Spec N = S;
+        N.variant = OEC_VARIANT_NAIVE;
+        bool have;
+        {
+            std::lock_guard<std::mutex> g(g_mu);
+            have = g_cache.count(spec_key(P, N, device)) > 0;
+        }
+        if (have) return run_variant<T>(P, in, out, sc, lo, hi, OEC_VARIANT_NAIVE, s);
+        return set_error(OEC_ERR_UNSUPPORTED, "%s: first AUTO call of this specialisation inside a stream capture "
+                         "(tune it with one call outside the capture)", P.name.c_str());
+    }
     // candidates: inline, unroll 2/4 along j and k, and every tiled configuration
     const int NC = 5 + N_TILE_CFGS;
     int cand[5 + N_TILE_CFGS], cfg[5 + N_TILE_CFGS];

@@ -241,3 +241,37 @@ def test_tiled_configurations(program, cfg, monkeypatch):
     host = synth.make_inputs(program, domain, seed=cfg)
     got, _ = run_jit(name, tp, host, domain, 7)
     check(got, oracle(tp, host, (0, 0, 0), domain), (0, 0, 0), domain)
+
+
+def test_first_auto_call_inside_capture():
+    """No tuning or compilation inside a stream capture: a builtin suite program's first AUTO call
+    on a new shape inside a capture runs its hand-written kernel (bit-identical); a text program
+    raises OEC_ERR_UNSUPPORTED until it has been called once outside the capture."""
+    import torch
+
+    oec = _oec()
+    program = "p_grad_c"
+    domain = (72, 40, 6)  # a shape no other test tunes
+    host = synth.make_inputs(program, domain, seed=9)
+    ins = [oec.field_from_host(host[s.name]) for s in synth.PROGRAMS[program].inputs]
+    outs = [oec.oec_field_create(domain, (0, 0, 0), (0, 0, 0)).fill(SENTINEL) for _ in synth.PROGRAMS[program].outputs]
+    s = torch.cuda.Stream()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        oec.oec_apply_program(program, ins, outs, [0.1125], (0, 0, 0), domain, 0)
+    g.replay()
+    torch.cuda.synchronize()
+    ref = run_gpu(program, host, domain, variant=2)  # hand-written inline kernel, outside capture
+    for o, f in zip(synth.PROGRAMS[program].outputs, outs):
+        assert np.array_equal(f.download(), ref[o].data)
+    # a text program's first AUTO call inside a capture
+    name = registered(text_of("uvbke"))
+    domain2 = (40, 24, 3)
+    h2 = synth.make_inputs("uvbke", domain2, seed=1)
+    ins2 = [oec.field_from_host(h2[s.name]) for s in synth.PROGRAMS["uvbke"].inputs]
+    outs2 = [oec.oec_field_create(domain2, (0, 0, 0), (0, 0, 0)) for _ in range(2)]
+    g2 = torch.cuda.CUDAGraph()
+    with pytest.raises(oec.OecError) as ei:
+        with torch.cuda.graph(g2, stream=s):
+            oec.oec_apply_program(name, ins2, outs2, None, (0, 0, 0), domain2, 0)
+    assert ei.value.status == 7
