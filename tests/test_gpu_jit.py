@@ -275,3 +275,32 @@ def test_first_auto_call_inside_capture():
         with torch.cuda.graph(g2, stream=s):
             oec.oec_apply_program(name, ins2, outs2, None, (0, 0, 0), domain2, 0)
     assert ei.value.status == 7
+
+
+def test_odd_pitch_torch_fields_auto():
+    """Torch-wrapped fields with an odd row pitch (not describable to TMA): AUTO tunes over the
+    non-TMA kernels only, the explicit tiled variant reports OEC_ERR_LAYOUT; results bit-identical."""
+    import torch
+
+    oec = _oec()
+    program = "nh_p_grad"
+    name = registered(text_of(program))
+    tp = dsl.parse(text_of(program))
+    domain = (37, 21, 5)
+    host = synth.make_inputs(program, domain, seed=13)
+    ins = []
+    for n in tp.inputs:
+        h = host[n]
+        shp = h.data.shape
+        t = torch.full((shp[0], shp[1], shp[2] + 3), float("nan"), dtype=torch.float64, device="cuda")[:, :, 1:1 + shp[2]]
+        t.copy_(torch.from_numpy(h.data))
+        ins.append(oec.oec_field_wrap(t, h.lb, h.ub, k_invariant=h.k_invariant))
+    outs = [oec.oec_field_create(domain, (0, 0, 0), (0, 0, 0)).fill(SENTINEL) for _ in tp.outputs]
+    oec.oec_apply_program(name, ins, outs, None, (0, 0, 0), domain, 0)
+    torch.cuda.synchronize()
+    ref = oracle(tp, host, (0, 0, 0), domain)
+    for o, f in zip(tp.outputs, outs):
+        assert np.array_equal(f.download(), ref[o])
+    with pytest.raises(oec.OecError) as ei:
+        oec.oec_apply_program(name, ins, outs, None, (0, 0, 0), domain, 7)
+    assert ei.value.status == 8
