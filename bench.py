@@ -497,13 +497,14 @@ def main():
         e2e = e2e_measure(oec, torch, hh, vh, dtr, domain, args.e2e_steps, world)
 
     # ---- remaining suite (evidence for SURVEY §8(a) a7; not part of the step) ----
-    suite_res = levels = f32_res = jit_res = pipe_res = None
+    suite_res = levels = f32_res = jit_res = pipe_res = paper_res = None
     if not args.no_suite and world == 1:
         suite_res = suite_measure(oec, torch, domain, l2, peak)
         levels = levels_measure(oec, torch, domain, l2, peak)
         f32_res = f32_measure(oec, torch, domain, l2, peak)
         jit_res = jit_measure(oec, torch, domain, l2, peak)
         pipe_res = pipeline_measure(oec, torch, domain, l2, peak)
+        paper_res = paper_sizes_measure(oec, torch, l2, peak)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -542,6 +543,8 @@ def main():
             res["jit"] = jit_res
         if pipe_res is not None:
             res["hdiff_pipeline"] = pipe_res
+        if paper_res is not None:
+            res["paper_sizes"] = paper_res
         print(json.dumps(res), flush=True)
     if decomp:
         dist.barrier()
@@ -697,6 +700,13 @@ def pipeline_measure(oec, torch, domain, l2, peak, reps=20):
     return {"us_per_step": us, "algorithmic_bytes": nbytes, "GB/s": nbytes / (us * 1e-6) / 1e9,
             "frac_of_hbm_peak": nbytes / (us * 1e-6) / 1e9 / peak, "pipelines": R,
             "note": "one rank (no neighbours); steps of R independent pipelines round-robin, fields > 4x L2"}
+
+
+def paper_sizes_measure(oec, torch, l2, peak):
+    """The paper's own problem sizes, 128x128x60 and 256x256x60, for every
+    program (default kernels: hand-written hdiff/vadv, the tuned compiler output for the suite)."""
+    return {"x".join(map(str, dom)): {p: program_measure(oec, torch, p, dom, l2, peak) for p in synth.ALL_PROGRAMS}
+            for dom in ((128, 128, 60), (256, 256, 60))}
 
 
 def levels_measure(oec, torch, domain, l2, peak):

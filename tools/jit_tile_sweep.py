@@ -18,6 +18,7 @@ def main():
     ap.add_argument("--domain", type=int, nargs=3, default=[128, 128, 80])
     ap.add_argument("--variant", type=int, default=7)
     ap.add_argument("--programs", nargs="*", default=None)
+    ap.add_argument("--dtype", default="f64", choices=["f64", "f32"])
     a = ap.parse_args()
     import torch
 
@@ -32,8 +33,11 @@ def main():
             continue
         with open(os.path.join(pdir, fn)) as f:
             name = oec.oec_program_create(f.read())
-        r = program_measure(oec, torch, fn[:-4], dom, l2, peak, a.variant, run_name=name)
-        print(json.dumps({"tile_cfg": os.environ.get("OEC_JIT_TILE_CFG", "0"), "variant": a.variant, "program": fn[:-4], "domain": list(dom),
+        import numpy as np
+
+        r = program_measure(oec, torch, fn[:-4], dom, l2, peak, a.variant, run_name=name,
+                            dtype=np.float32 if a.dtype == "f32" else np.float64)
+        print(json.dumps({"tile_cfg": os.environ.get("OEC_JIT_TILE_CFG", "0"), "variant": a.variant, "dtype": a.dtype, "program": fn[:-4], "domain": list(dom),
                           "us": round(r["us_per_launch"], 2), "frac": round(r["frac_of_hbm_peak"], 3)}), flush=True)
         oec.oec_program_destroy(name)
 
