@@ -270,7 +270,9 @@ def test_vadv_inline_level_and_unroll_rejected():
 
 
 def test_hdiff_large_config_ragged():
-    # >= 2M points selects the wide-tile hdiff configuration (V=4, JB=2); ragged in i and j
-    _check("hdiff", (1031, 1029, 3), seed=5)
-    _check("hdiff", (333, 6301, 1), seed=6, out_halo=(2, 2, 0))
-    _check("hdiff", (517, 1000, 5), seed=7, order=(0, 1, 2))
+    # >= 8M points selects the wide-tile hdiff configuration (V=4, JB=2); ragged in i and j
+    _check("hdiff", (1031, 1029, 9), seed=5)
+    _check("hdiff", (333, 6301, 4), seed=6, out_halo=(2, 2, 0))
+    _check("hdiff", (517, 1000, 17), seed=7, order=(0, 1, 2))
+    # just below the threshold: the small-tile configuration on a multi-million-point domain
+    _check("hdiff", (1031, 1029, 3), seed=8)

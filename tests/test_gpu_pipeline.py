@@ -91,7 +91,7 @@ def check(ranks, ref, T):
     ((200, 50, 2), 3, 2, 5),
     ((33, 20, 2), 4, 1, 3),      # narrow sub-domains: every tile is a boundary tile
     ((9, 8, 2), 2, 2, 2),        # sub-domains of 4-5 cells
-    ((2048, 700, 3), 2, 1, 2),   # > 2M points per rank: the large tile configuration
+    ((4096, 1100, 4), 2, 1, 2),  # > 8M points per rank: the large tile configuration
 ])
 @pytest.mark.parametrize("dtype", [np.float64, np.float32])
 def test_pipeline_matches_oracle_steps(gdom, px, py, T, dtype):
