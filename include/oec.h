@@ -242,11 +242,19 @@ int32_t oec_last_launch_count(void);
  * operator's iteration domain is the bounding box of what its own readers need and a stored
  * result is needed on the domain.
  *
- * Variants (oec_apply_program): AUTO / NAIVE = inline, one generated kernel, one thread
- * per point, every operator recomputed at every offset its readers use, each (operator, offset)
- * and (input, offset) evaluated once per thread (CSE); UNROLL2 / UNROLL4 = inline +
- * unroll along j; UNFUSED = the original level, one kernel per live operator over
- * its inferred domain, temporaries in a library device workspace (single stream at a time).
+ * Variants (oec_apply_program): NAIVE = inline, one generated kernel, one thread per
+ * point, every operator recomputed at every offset its readers use, each (operator, offset) and
+ * (input, offset) evaluated once per thread (CSE); UNROLL2 / UNROLL4 = inline + unroll along
+ * j, UNROLL2_K / UNROLL4_K along k; TILED = the B200 execution model (TMA-staged
+ * input boxes in a shared-memory ring, persistent CTAs); UNFUSED = the original level, one
+ * kernel per live operator over its inferred domain, temporaries in a library device workspace
+ * (single stream at a time); AUTO = empirical tuning: the first call of a specialisation
+ * times inline, the unrolled variants and four tiled configurations on the caller's stream
+ * (synchronising it; every candidate writes the same bits) and caches the fastest.  Inside a
+ * stream capture AUTO never tunes or compiles: it runs the inline kernel if already compiled,
+ * else returns OEC_ERR_UNSUPPORTED.  The builtin suite programs' AUTO uses this compiler on their
+ * stencil-language definitions (and their hand-written kernels when it returns
+ * OEC_ERR_UNSUPPORTED).
  * Kernels are generated with the domain size and all strides as constants, compiled by
  * NVRTC for sm_100a on first use of a (program, dtype, variant, size, strides, device) and
  * cached for the life of the process; the first call of a specialisation must not be inside a
