@@ -1,4 +1,6 @@
 cd "$GRAFT_REPO_ROOT" || exit 1
 mkdir -p gpurun_out
-timeout 1500 python -m pytest tests -m gpu -q --timeout 600 > gpurun_out/pytest_final.txt 2>&1; echo "exit $?" >> gpurun_out/pytest_final.txt
-timeout 300 python __graft_entry__.py --smoke > gpurun_out/smoke_final.txt 2>&1; echo "exit $?" >> gpurun_out/smoke_final.txt
+: > gpurun_out/s3.jsonl
+for rep in 1 2 3; do for v in s4 s3; do for dom in "128 128 80" "128 128 60"; do
+  OEC_LIB_PATH=tune/$v.so timeout 300 python tools/kernel_bench.py --programs vadv --domain $dom --tag $v >> gpurun_out/s3.jsonl 2>&1
+done; done; done
