@@ -242,34 +242,47 @@ class StepSet:
         return sum(int(np.prod([f.ub[d] - f.lb[d] for d in range(3)])) * 8 for f in fs)
 
 
-def fused_pipelines(oec, dist, sets, domain, world, rank, dev_index):
+def fused_pipelines(oec, dist, sets, domain, world, rank, dev_index, agree):
     """N > 1, --exchange fused: one oec_hdiff_pipeline per rotating set over this rank's j-slab of
     the global 128 x 128N x 80 domain (x0 = the set's hdiff input with its halo, x1 a copy: the
     global outer halo stays constant); fields and signal pads are exported with CUDA IPC, the
-    handles all-gathered, and every pipeline registers its j-neighbours' (imported) fields."""
-    gdom = (domain[0], domain[1] * world, domain[2])
-    mine = []
-    for s in sets:
-        x1 = oec.oec_field_create(domain, (2, 2, 0), (2, 2, 0))
-        x1.view().copy_(s.h_in.view())
-        s.x1 = x1
-        s.pipe = oec.HdiffPipeline(gdom, 1, world, rank, s.h_cf, s.h_in, x1)
-        pad, _ = s.pipe.signal_pad()
-        mine.append(dict(x0=oec.oec_ipc_export(s.h_in.desc.data), x1=oec.oec_ipc_export(x1.desc.data),
-                         pad=oec.oec_ipc_export(pad), desc=oec.field_descriptor(s.h_in)))
+    handles all-gathered, and every pipeline registers its j-neighbours' (imported) fields.
+    Each phase ends with agree(ok) (a MIN over ranks), so every rank takes the same path; returns
+    None on success, else the reason."""
     import torch
 
-    torch.cuda.synchronize()
+    gdom = (domain[0], domain[1] * world, domain[2])
+    mine, err = [], None
+    try:  # phase 1: local pipelines and IPC exports
+        for s in sets:
+            x1 = oec.oec_field_create(domain, (2, 2, 0), (2, 2, 0))
+            x1.view().copy_(s.h_in.view())
+            s.x1 = x1
+            s.pipe = oec.HdiffPipeline(gdom, 1, world, rank, s.h_cf, s.h_in, x1)
+            pad, _ = s.pipe.signal_pad()
+            mine.append(dict(x0=oec.oec_ipc_export(s.h_in.desc.data), x1=oec.oec_ipc_export(x1.desc.data),
+                             pad=oec.oec_ipc_export(pad), desc=oec.field_descriptor(s.h_in)))
+        torch.cuda.synchronize()
+    except Exception as e:
+        err = f"{type(e).__name__}: {e}"
+    if not agree(err is None):
+        return err or "pipeline setup failed on another rank"
     everyone = [None] * world
     dist.all_gather_object(everyone, mine)
-    for q in (rank - 1, rank + 1):
-        if not 0 <= q < world:
-            continue
-        for si, s in enumerate(sets):
-            Q = everyone[q][si]
-            p0, p1, pp = (oec.oec_ipc_import(*Q[k]) for k in ("x0", "x1", "pad"))
-            s.pipe.set_peer(q, oec.field_at(p0, Q["desc"], dev_index), oec.field_at(p1, Q["desc"], dev_index), pp)
+    try:  # phase 2: import the j-neighbours' memory
+        for q in (rank - 1, rank + 1):
+            if not 0 <= q < world:
+                continue
+            for si, s in enumerate(sets):
+                Q = everyone[q][si]
+                p0, p1, pp = (oec.oec_ipc_import(*Q[k]) for k in ("x0", "x1", "pad"))
+                s.pipe.set_peer(q, oec.field_at(p0, Q["desc"], dev_index), oec.field_at(p1, Q["desc"], dev_index), pp)
+    except Exception as e:
+        err = f"{type(e).__name__}: {e}"
+    if not agree(err is None):
+        return err or "peer import failed on another rank"
     dist.barrier()
+    return None
 
 
 def main():
@@ -346,18 +359,17 @@ def main():
     sets = [first] + [StepSet(oec, hh, vh, domain) for _ in range(R - 1)]
     fused_note = None
     if fused:
-        try:
-            fused_pipelines(oec, dist, sets, domain, world, rank, dev_index)
-            ok = 1
-        except Exception as e:  # e.g. no peer access: every rank falls back to the NCCL exchange
-            ok, fused_note = 0, f"fused pipeline unavailable ({type(e).__name__}: {e}); NCCL exchange used"
-        flag = torch.tensor([ok], dtype=torch.int32, device="cuda" if args.dist_backend == "nccl" else "cpu")
-        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
-        if int(flag.item()) == 0:
+        def agree(ok):
+            flag = torch.tensor([1 if ok else 0], dtype=torch.int32, device="cuda" if args.dist_backend == "nccl" else "cpu")
+            dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+            return int(flag.item()) == 1
+
+        why = fused_pipelines(oec, dist, sets, domain, world, rank, dev_index, agree)
+        if why is not None:  # e.g. no peer access: every rank falls back to the NCCL exchange
             if args.dist_backend != "nccl":
-                raise SystemExit(fused_note or "fused pipeline failed on another rank")
+                raise SystemExit(f"fused pipeline unavailable: {why}")
             fused = False
-            fused_note = fused_note or "fused pipeline failed on another rank; NCCL exchange used"
+            fused_note = f"fused pipeline unavailable ({why}); NCCL exchange used"
             pg = dist.distributed_c10d._get_default_group()
             dec = oec.oec_decomp_create((domain[0], domain[1] * world, domain[2]), 1, world, rank,
                                         pg._get_backend(torch.device("cuda", dev_index))._comm_ptr())
