@@ -214,7 +214,7 @@ def test_branch_free_reciprocal_is_ieee():
 
 @pytest.mark.parametrize("K", [84, 85, 100, 128, 129, 200, 260])
 def test_vadv_tall_columns_every_kernel(K):
-    # K <= 84: vadv_ws2 (c', d', u_pos in TMEM); <= 128: vadv_ws (c', d' in TMEM); <= ~190: vadv_tma
+    # K <= 84: vadv_sp (c', d', u_pos in TMEM); <= 128: vadv_ws (c', d' in TMEM); <= ~190: vadv_tma
     # (c', d' in shared memory); taller: the register kernel with a global c'/d' workspace
     _check("vadv", (130, 3, K), seed=K)
 
