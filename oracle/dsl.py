@@ -335,6 +335,9 @@ def _combine(op, x, kids, sel):
         return -kids[0]
     if op == "bin":
         p, q = kids[1], kids[2]
+        cnt = getattr(sel, "census_cnt", None)
+        if cnt is not None and tracer is None and x[2][0] == "lit" and x[3][0] == "lit":
+            cnt["arith"] += 1  # e.g. (7.0 / 12.0): an operation of the program text (census, R15)
         return {"+": lambda: p + q, "-": lambda: p - q, "*": lambda: p * q, "/": lambda: p / q}[x[1]]()
     if op == "cmp":
         p, q = kids[1], kids[2]

@@ -89,6 +89,7 @@ def census(prog: Program) -> Dict[str, int]:
         cnt["if"] += 1
         return _T(cnt)
 
+    sel.census_cnt = cnt  # kdiv / literal ops of the stencil language count as arithmetic ops
     s = {k: 1.0 for k in prog.scalars}
     for ap in prog.applies:
         ap.fn(a, s, sel)
@@ -98,6 +99,16 @@ def census(prog: Program) -> Dict[str, int]:
         "outputs": len(prog.outputs),
         **cnt,
     }
+
+
+def kdiv(sel, n: float, d: float) -> float:
+    """A constant written in the definition as the quotient n / d (e.g. the PPM weight 7/12):
+    numerically the IEEE double n / d, and for the census (Table II) one arithmetic operation,
+    as the operation appears in the program text (reading R15)."""
+    cnt = getattr(sel, "census_cnt", None)
+    if cnt is not None:
+        cnt["arith"] += 1
+    return n / d
 
 
 def accesses(ap: Apply, scalars: Sequence[str]) -> List[Tuple[str, int, int, int]]:

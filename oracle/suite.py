@@ -9,9 +9,9 @@ reconstructions from the public FV3 sources [EXT] (DESIGN.md readings R12-R17); 
 not in PAPER.md at all (north_star; COSMO fast-waves u/v [EXT], reading R17).
 
 Pins (tests/test_oracle_suite.py):
-  * census vs Table II -- uvbke, p_grad_c and nh_p_grad match every column exactly; the three
-    fvtp2d programs match dims / apply ops / inputs-outputs / control flow, and differ in arith
-    and access counts by the amounts listed in DESIGN.md (reading R15);
+  * census vs Table II -- all six programs match every column exactly (the fvtp2d PPM written
+    as enumerated in DESIGN.md reading R15);
+  * closed-form flux divergence of fvtp2d_qi / fvtp2d_qj (linear q, uniform Courant number);
   * closed forms / special cases for every program (constant, linear and flat fields);
   * unfused (materialised) == fused (inlined) bitwise, extents == brute-force touched set.
   The VALUES of these programs are "parity unpinned" against the paper: PAPER.md prints none.
@@ -22,7 +22,7 @@ operation order the CUDA kernels reproduce.
 """
 from __future__ import annotations
 
-from oracle.stencil import Apply, Program
+from oracle.stencil import Apply, Program, kdiv
 
 # ---------------------------------------------------------------------------------------------
 # uvbke (FV3 d_sw.F90 ub/vb)  -- Table II: 2 / 2 / 4/2 / 12 / 12 / -
@@ -109,10 +109,14 @@ NH_P_GRAD = Program(
 # ---------------------------------------------------------------------------------------------
 # fv_tp_2d (FV3 tp_core.F90) split into the paper's three programs.  The 1D PPM flux of q
 # through the face at the lower side of cell (i,j) with Courant number c (reading R14):
-#   al = p1 (q[-1] + q) + p2 (q[-2] + q[+1]),   p1 = 7/12, p2 = -1/12   (4th-order edge value)
+#   al = (7/12) (q[-1] + q) - (1/12) (q[-2] + q[+1])                  (4th-order edge value)
 #   bl = al - q,  br = al[+1] - q
 #   flux = c > 0 ? q[-1] + (1 - c)(br[-1] - c (bl[-1] + br[-1]))       (upwind `if`)
 #               : q    + (1 + c)(bl     + c (bl     + br    ))
+# Written as the paper's programs are counted (reading R15): the weights are the quotients
+# 7/12 and 1/12 of the text (two arithmetic operations), and the condition and each branch
+# region of the `if` read c themselves (three accesses).  Numerically this is the same as
+# literal weights p1 = 7/12, p2 = -1/12 and one read of c: a + (-p) x == a - p x exactly.
 # ---------------------------------------------------------------------------------------------
 P1 = 7.0 / 12.0
 P2 = -1.0 / 12.0
@@ -123,19 +127,21 @@ def _ppm(q: str, c: str, al: str, bl: str, br: str, flux: str, dim: str):
         return (0, d) if dim == "j" else (d, 0)
 
     def f_al(a, s, sel):
-        return P1 * (a(q, *o(-1)) + a(q)) + P2 * (a(q, *o(-2)) + a(q, *o(1)))
+        return kdiv(sel, 7.0, 12.0) * (a(q, *o(-1)) + a(q)) - kdiv(sel, 1.0, 12.0) * (a(q, *o(-2)) + a(q, *o(1)))
 
     def f_blbr(a, s, sel):
         qq = a(q)
         return a(al) - qq, a(al, *o(1)) - qq
 
     def f_flux(a, s, sel):
-        cc = a(c)
+        cc = a(c)  # the condition's read
+        c1 = a(c)  # the c > 0 region's read
+        c2 = a(c)  # the else region's read
         blm, brm = a(bl, *o(-1)), a(br, *o(-1))
         bl0, br0 = a(bl), a(br)
         return sel(cc > 0.0,
-                   a(q, *o(-1)) + (1.0 - cc) * (brm - cc * (blm + brm)),
-                   a(q) + (1.0 + cc) * (bl0 + cc * (bl0 + br0)))
+                   a(q, *o(-1)) + (1.0 - c1) * (brm - c1 * (blm + brm)),
+                   a(q) + (1.0 + c2) * (bl0 + c2 * (bl0 + br0)))
 
     return (Apply((al,), f_al), Apply((bl, br), f_blbr), Apply((flux,), f_flux))
 

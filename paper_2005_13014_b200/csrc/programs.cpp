@@ -79,7 +79,8 @@ store v_t -> v_out
 )OEC";
     case OEC_PROG_FVTP2D_QI:
         return R"OEC(# fvtp2d_qi (FV3 tp_core fv_tp_2d, j-direction PPM flux; Table II: 5 applies, 5/2, if) -- DESIGN.md R14/R15.
-# PPM edge value: p1 = 7/12, p2 = -1/12 (binary64 literals of those quotients).
+# PPM edge value (7/12) (q[-1] + q) - (1/12) (q[-2] + q[1]); c read by the condition and by each
+# select branch (the census of Table II, DESIGN.md R15).
 program fvtp2d_qi_text
 input q
 input cry
@@ -88,18 +89,20 @@ input area : ij
 input ra_y
 output q_i
 output fy2
-apply al = 0.5833333333333334 * (q[0,-1,0] + q) + -0.08333333333333333 * (q[0,-2,0] + q[0,1,0])
+apply al = (7.0 / 12.0) * (q[0,-1,0] + q) - (1.0 / 12.0) * (q[0,-2,0] + q[0,1,0])
 apply bl, br {
     qq = q
     return al - qq, al[0,1,0] - qq
 }
 apply fy2_t {
     c = cry
+    c1 = cry
+    c2 = cry
     blm = bl[0,-1,0]
     brm = br[0,-1,0]
     bl0 = bl
     br0 = br
-    return select(c > 0.0, q[0,-1,0] + (1.0 - c) * (brm - c * (blm + brm)), q + (1.0 + c) * (bl0 + c * (bl0 + br0)))
+    return select(c > 0.0, q[0,-1,0] + (1.0 - c1) * (brm - c1 * (blm + brm)), q + (1.0 + c2) * (bl0 + c2 * (bl0 + br0)))
 }
 apply fyy = yfx * fy2_t
 apply q_i_t = (q * area + fyy - fyy[0,1,0]) / ra_y
@@ -118,31 +121,35 @@ input ra_x
 output q_j
 output fx
 output fx2
-apply al = 0.5833333333333334 * (q_i[-1,0,0] + q_i) + -0.08333333333333333 * (q_i[-2,0,0] + q_i[1,0,0])
+apply al = (7.0 / 12.0) * (q_i[-1,0,0] + q_i) - (1.0 / 12.0) * (q_i[-2,0,0] + q_i[1,0,0])
 apply bl, br {
     qq = q_i
     return al - qq, al[1,0,0] - qq
 }
 apply fx_t {
     c = crx
+    c1 = crx
+    c2 = crx
     blm = bl[-1,0,0]
     brm = br[-1,0,0]
     bl0 = bl
     br0 = br
-    return select(c > 0.0, q_i[-1,0,0] + (1.0 - c) * (brm - c * (blm + brm)), q_i + (1.0 + c) * (bl0 + c * (bl0 + br0)))
+    return select(c > 0.0, q_i[-1,0,0] + (1.0 - c1) * (brm - c1 * (blm + brm)), q_i + (1.0 + c2) * (bl0 + c2 * (bl0 + br0)))
 }
-apply al2 = 0.5833333333333334 * (q[-1,0,0] + q) + -0.08333333333333333 * (q[-2,0,0] + q[1,0,0])
+apply al2 = (7.0 / 12.0) * (q[-1,0,0] + q) - (1.0 / 12.0) * (q[-2,0,0] + q[1,0,0])
 apply bl2, br2 {
     qq = q
     return al2 - qq, al2[1,0,0] - qq
 }
 apply fx2_t {
     c = crx
+    c1 = crx
+    c2 = crx
     blm = bl2[-1,0,0]
     brm = br2[-1,0,0]
     bl0 = bl2
     br0 = br2
-    return select(c > 0.0, q[-1,0,0] + (1.0 - c) * (brm - c * (blm + brm)), q + (1.0 + c) * (bl0 + c * (bl0 + br0)))
+    return select(c > 0.0, q[-1,0,0] + (1.0 - c1) * (brm - c1 * (blm + brm)), q + (1.0 + c2) * (bl0 + c2 * (bl0 + br0)))
 }
 apply fx1 = xfx * fx2_t
 apply q_j_t = (q * area + fx1 - fx1[1,0,0]) / ra_x
@@ -162,18 +169,20 @@ input mfx
 input mfy
 output fx_out
 output fy_out
-apply al = 0.5833333333333334 * (q_j[0,-1,0] + q_j) + -0.08333333333333333 * (q_j[0,-2,0] + q_j[0,1,0])
+apply al = (7.0 / 12.0) * (q_j[0,-1,0] + q_j) - (1.0 / 12.0) * (q_j[0,-2,0] + q_j[0,1,0])
 apply bl, br {
     qq = q_j
     return al - qq, al[0,1,0] - qq
 }
 apply fy {
     c = cry
+    c1 = cry
+    c2 = cry
     blm = bl[0,-1,0]
     brm = br[0,-1,0]
     bl0 = bl
     br0 = br
-    return select(c > 0.0, q_j[0,-1,0] + (1.0 - c) * (brm - c * (blm + brm)), q_j + (1.0 + c) * (bl0 + c * (bl0 + br0)))
+    return select(c > 0.0, q_j[0,-1,0] + (1.0 - c1) * (brm - c1 * (blm + brm)), q_j + (1.0 + c2) * (bl0 + c2 * (bl0 + br0)))
 }
 apply fx_t = 0.5 * (fx + fx2) * mfx
 apply fy_t = 0.5 * (fy + fy2) * mfy

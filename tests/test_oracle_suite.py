@@ -16,24 +16,69 @@ from synth import HostField
 SUITE = synth.SUITE
 
 
-@pytest.mark.parametrize("name", ["uvbke", "p_grad_c", "nh_p_grad"])
+@pytest.mark.parametrize("name", sorted(suite.TABLE_II))
 def test_census_matches_table_ii_exactly(name):
+    # every column of Table II for all six programs; the compare of the fvtp2d upwind
+    # `if` counts as an arithmetic operation (reading R15)
     dims, applies, n_in, n_out, arith, access, cf = suite.TABLE_II[name]
     c = st.census(suite.PROGRAMS[name])
-    assert (c["applies"], c["inputs"], c["outputs"], c["arith"], c["access"], c["if"] > 0) == (
+    assert (c["applies"], c["inputs"], c["outputs"], c["arith"] + c["cmp"], c["access"], c["if"] > 0) == (
         applies, n_in, n_out, arith, access, cf)
 
 
-@pytest.mark.parametrize("name", ["fvtp2d_qi", "fvtp2d_qj", "fvtp2d_flux"])
-def test_census_fvtp2d_structure(name):
-    # apply ops, inputs/outputs and control flow match Table II; the arith/access counts of the
-    # reconstructed PPM differ by a fixed amount per PPM flux (reading R15)
-    dims, applies, n_in, n_out, arith, access, cf = suite.TABLE_II[name]
-    c = st.census(suite.PROGRAMS[name])
-    assert (c["applies"], c["inputs"], c["outputs"], c["if"] > 0) == (applies, n_in, n_out, cf)
-    n_ppm = 2 if name == "fvtp2d_qj" else 1
-    assert c["arith"] + c["cmp"] == arith - 2 * n_ppm
-    assert c["access"] == access - 2 * n_ppm
+def _ppm_candidate(weights_as_quotients, c_reads):
+    """One writing of the PPM flux program (R15 enumeration): the weights as literals or
+    as the quotients 7/12, 1/12 of the text; c read once ('shared'), by the condition and each
+    branch region ('regions'), or at every use ('uses')."""
+    def prog(q, c, dim):
+        def o(d):
+            return (0, d) if dim == "j" else (d, 0)
+
+        def f_al(a, s, sel):
+            if weights_as_quotients:
+                return st.kdiv(sel, 7.0, 12.0) * (a(q, *o(-1)) + a(q)) - st.kdiv(sel, 1.0, 12.0) * (a(q, *o(-2)) + a(q, *o(1)))
+            return suite.P1 * (a(q, *o(-1)) + a(q)) + suite.P2 * (a(q, *o(-2)) + a(q, *o(1)))
+
+        def f_blbr(a, s, sel):
+            qq = a(q)
+            return a("al", *o(0)) - qq, a("al", *o(1)) - qq
+
+        def f_flux(a, s, sel):
+            cc = a(c)
+            if c_reads == "shared":
+                c1 = c2 = c3 = c4 = cc
+            elif c_reads == "regions":
+                c1 = c2 = a(c)  # the c > 0 region's read
+                c3 = c4 = a(c)  # the else region's read
+            else:
+                c1, c2, c3, c4 = a(c), a(c), a(c), a(c)
+            blm, brm = a("bl", *o(-1)), a("br", *o(-1))
+            bl0, br0 = a("bl"), a("br")
+            return sel(cc > 0.0, a(q, *o(-1)) + (1.0 - c1) * (brm - c2 * (blm + brm)),
+                       a(q) + (1.0 + c3) * (bl0 + c4 * (bl0 + br0)))
+
+        return (st.Apply(("al",), f_al), st.Apply(("bl", "br"), f_blbr), st.Apply(("f",), f_flux))
+    return prog
+
+
+def test_fvtp2d_census_enumeration():
+    # the enumeration behind reading R15: the extra arithmetic / access operations of each writing
+    # of one PPM flux over the minimal one; only "quotient weights + c read per region" gives
+    # Table II's +2 / +2 per PPM flux (27/23, 49/39, 28/22 in the three programs)
+    def counts(wq, cr):
+        p = st.Program("ppm", ("q", "c"), (("f", "f"),), _ppm_candidate(wq, cr)("q", "c", "j"))
+        c = st.census(p)
+        return c["arith"] + c["cmp"], c["access"]
+
+    base = counts(False, "shared")
+    assert base == (20, 14)
+    table = {(wq, cr): tuple(x - y for x, y in zip(counts(wq, cr), base))
+             for wq in (False, True) for cr in ("shared", "regions", "uses")}
+    assert table == {(False, "shared"): (0, 0), (False, "regions"): (0, 2), (False, "uses"): (0, 4),
+                     (True, "shared"): (2, 0), (True, "regions"): (2, 2), (True, "uses"): (2, 4)}
+    # the suite's PPM is that writing
+    qi = st.census(suite.PROGRAMS["fvtp2d_qi"])
+    assert (qi["arith"] + qi["cmp"], qi["access"]) == (base[0] + 2 + 5, base[1] + 2 + 7)
 
 
 def _dims_used(prog):
@@ -230,6 +275,42 @@ def test_qi_uniform_state_closed_form():
     r = _unf("fvtp2d_qi", f, domain)
     # (q*area + F) - F rounds once more than q*area: equal to ~1 ulp
     assert np.allclose(r["q_i"].data, 0.625 * f["area"].data / f["ra_y"].data, rtol=4e-16, atol=0)
+
+
+def test_qi_flux_divergence_closed_form():
+    # linear q = j, uniform cry = c and yfx = Y: the PPM flux is exact, fy2(j) = j - 1/2 - c/2, so
+    # fyy(j) - fyy(j+1) = -Y and q_i = (j area - Y) / ra_y.  The sign of the divergence is pinned:
+    # fyy(j+1) - fyy(j) would give (j area + Y) / ra_y.  Both branches of the upwind `if`.
+    domain = (3, 6, 2)
+    j = np.arange(6).reshape(1, 6, 1)
+    for c, Y in ((0.25, 0.5), (-0.375, -0.75)):
+        f = synth.make_inputs("fvtp2d_qi", domain, seed=21)
+        f["q"].data[:] = _grid(f["q"])[1]
+        f["cry"].data[:] = c
+        f["yfx"].data[:] = Y
+        r = _unf("fvtp2d_qi", f, domain)
+        area = f["area"].data[:, 0:6, :]
+        ra = f["ra_y"].data[:, 0:6, :]
+        assert np.allclose(r["q_i"].data, (j * area - Y) / ra, rtol=1e-14, atol=1e-14)
+        assert not np.allclose(r["q_i"].data, (j * area + Y) / ra, rtol=1e-3, atol=1e-3)
+
+
+def test_qj_flux_divergence_closed_form():
+    # the i analogue for q_j: q = i, uniform crx = c, xfx = X: fx2(i) = i - 1/2 - c/2,
+    # q_j = (i area - X) / ra_x; fx (the flux of q_i) is independent of q
+    domain = (6, 3, 2)
+    i = np.arange(6).reshape(1, 1, 6)
+    for c, X in ((0.375, 0.25), (-0.125, -0.5)):
+        f = synth.make_inputs("fvtp2d_qj", domain, seed=22)
+        f["q"].data[:] = _grid(f["q"])[0]
+        f["crx"].data[:] = c
+        f["xfx"].data[:] = X
+        r = _unf("fvtp2d_qj", f, domain)
+        area = f["area"].data[:, :, 0:6]
+        ra = f["ra_x"].data[:, :, 0:6]
+        assert np.allclose(r["fx2"].data, i - 0.5 - c / 2, rtol=0, atol=2e-15)
+        assert np.allclose(r["q_j"].data, (i * area - X) / ra, rtol=1e-14, atol=1e-14)
+        assert not np.allclose(r["q_j"].data, (i * area + X) / ra, rtol=1e-3, atol=1e-3)
 
 
 def test_qj_uniform_state_closed_form():
