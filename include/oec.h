@@ -161,6 +161,10 @@ oec_status oec_program_info(const char *program, int32_t *n_inputs, int32_t *n_o
 oec_status oec_program_input(const char *program, int32_t idx, const char **name, int64_t lo[3], int64_t hi[3],
                              int32_t *k_invariant);
 
+/* a1 as SURVEY §8(b) names it: the access extent [lo, hi) of input `input_idx` relative to the
+ * domain (shape inference) -- the same lo / hi as oec_program_input. */
+oec_status oec_program_extent(const char *program, int32_t input_idx, int64_t lo[3], int64_t hi[3]);
+
 /* Name of output `idx` / scalar `idx` (static strings). */
 oec_status oec_program_output(const char *program, int32_t idx, const char **name);
 oec_status oec_program_scalar(const char *program, int32_t idx, const char **name, double *default_value);

@@ -49,10 +49,27 @@ def build(force: bool = False, verbose: bool = False, defines=(), out: str = LIB
     builds written to `out`; the product build uses the defaults in the sources."""
     if not force and out == LIB and not defines and not _stale():
         return LIB
-    cmd = [NVCC, *ARCH, *FLAGS, *(["-Xptxas", "-v"] if verbose else []), *["-D" + d for d in defines], *sources(),
-           "-o", out + ".tmp", "-ldl"]
-    subprocess.check_call(cmd)
+    # one nvcc per translation unit in parallel (no device code crosses TUs), then one link
+    from concurrent.futures import ThreadPoolExecutor
+
+    cflags = [f for f in FLAGS if f != "-shared"]
+    objdir = out + ".objs"
+    os.makedirs(objdir, exist_ok=True)
+
+    def compile_one(src):
+        obj = os.path.join(objdir, os.path.basename(src) + ".o")
+        cmd = [NVCC, *ARCH, *cflags, *(["-Xptxas", "-v"] if verbose else []), *["-D" + d for d in defines], "-c", src,
+               "-o", obj]
+        subprocess.check_call(cmd)
+        return obj
+
+    with ThreadPoolExecutor(max_workers=max(1, min(len(sources()), os.cpu_count() or 1))) as ex:
+        objs = list(ex.map(compile_one, sources()))
+    subprocess.check_call([NVCC, *ARCH, "-shared", *objs, "-o", out + ".tmp", "-ldl"])
     os.replace(out + ".tmp", out)
+    for o in objs:
+        os.remove(o)
+    os.rmdir(objdir)
     return out
 
 

@@ -10,6 +10,7 @@
 #include <dlfcn.h>
 #include <string.h>
 
+#include <algorithm>
 #include <mutex>
 #include <vector>
 
@@ -25,40 +26,51 @@ struct oec_decomp {
 namespace oec {
 namespace {
 
+// box kernels: x threads along i, grid.y over j, grid.z over k (grid-stride in every dimension);
+// no per-element integer division
 template <class T>
 __global__ void pack_kernel(FVT<T> src, Box b, T *buf) {
-    const long long ni = b.hi[0] - b.lo[0], nj = b.hi[1] - b.lo[1], nk = b.hi[2] - b.lo[2];
-    const long long n = ni * nj * nk;
-    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n; t += (long long)gridDim.x * blockDim.x) {
-        const int i = b.lo[0] + (int)(t % ni), j = b.lo[1] + (int)((t / ni) % nj), k = b.lo[2] + (int)(t / (ni * nj));
-        buf[t] = src.p[i + j * src.sj + k * src.sk];
-    }
+    const int ni = b.hi[0] - b.lo[0], nj = b.hi[1] - b.lo[1], nk = b.hi[2] - b.lo[2];
+    for (int k = blockIdx.z; k < nk; k += gridDim.z)
+        for (int j = blockIdx.y; j < nj; j += gridDim.y) {
+            const T *row = src.p + (b.lo[1] + j) * (long long)src.sj + (b.lo[2] + k) * (long long)src.sk + b.lo[0];
+            T *dst = buf + ((long long)k * nj + j) * ni;
+            for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < ni; i += gridDim.x * blockDim.x) dst[i] = row[i];
+        }
 }
 template <class T>
 __global__ void unpack_kernel(const T *buf, Box b, FOT<T> dst) {
-    const long long ni = b.hi[0] - b.lo[0], nj = b.hi[1] - b.lo[1], nk = b.hi[2] - b.lo[2];
-    const long long n = ni * nj * nk;
-    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n; t += (long long)gridDim.x * blockDim.x) {
-        const int i = b.lo[0] + (int)(t % ni), j = b.lo[1] + (int)((t / ni) % nj), k = b.lo[2] + (int)(t / (ni * nj));
-        dst.p[i + j * dst.sj + k * dst.sk] = buf[t];
-    }
+    const int ni = b.hi[0] - b.lo[0], nj = b.hi[1] - b.lo[1], nk = b.hi[2] - b.lo[2];
+    for (int k = blockIdx.z; k < nk; k += gridDim.z)
+        for (int j = blockIdx.y; j < nj; j += gridDim.y) {
+            T *row = dst.p + (b.lo[1] + j) * (long long)dst.sj + (b.lo[2] + k) * (long long)dst.sk + b.lo[0];
+            const T *src = buf + ((long long)k * nj + j) * ni;
+            for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < ni; i += gridDim.x * blockDim.x) row[i] = src[i];
+        }
 }
 template <class T>
 __global__ void box_copy_kernel(FVT<T> src, FOT<T> dst, Box b) {
-    const long long ni = b.hi[0] - b.lo[0], nj = b.hi[1] - b.lo[1], nk = b.hi[2] - b.lo[2];
-    const long long n = ni * nj * nk;
-    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n; t += (long long)gridDim.x * blockDim.x) {
-        const int i = b.lo[0] + (int)(t % ni), j = b.lo[1] + (int)((t / ni) % nj), k = b.lo[2] + (int)(t / (ni * nj));
-        dst.p[i + j * dst.sj + k * dst.sk] = src.p[i + j * src.sj + k * src.sk];
-    }
+    const int ni = b.hi[0] - b.lo[0], nj = b.hi[1] - b.lo[1], nk = b.hi[2] - b.lo[2];
+    for (int k = blockIdx.z; k < nk; k += gridDim.z)
+        for (int j = blockIdx.y; j < nj; j += gridDim.y) {
+            const long long j_ = b.lo[1] + j, k_ = b.lo[2] + k;
+            const T *r = src.p + j_ * src.sj + k_ * src.sk + b.lo[0];
+            T *w = dst.p + j_ * dst.sj + k_ * dst.sk + b.lo[0];
+            for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < ni; i += gridDim.x * blockDim.x) w[i] = r[i];
+        }
 }
 
 long long box_volume(const Box &b) {
     return (long long)(b.hi[0] - b.lo[0]) * (b.hi[1] - b.lo[1]) * (b.hi[2] - b.lo[2]);
 }
-unsigned grid_for(long long n) {
-    long long g = (n + 255) / 256;
-    return (unsigned)(g < 1 ? 1 : (g > 148 * 16 ? 148 * 16 : g));
+// threads along i (up to 256), rows over y/z, at most ~16 CTAs per SM in total
+void grid_for(const Box &b, dim3 *g, dim3 *t) {
+    const int ni = b.hi[0] - b.lo[0], nj = b.hi[1] - b.lo[1], nk = b.hi[2] - b.lo[2];
+    t->x = ni >= 256 ? 256 : ni >= 128 ? 128 : ni >= 64 ? 64 : 32;
+    g->x = (unsigned)std::min(8, (ni + (int)t->x - 1) / (int)t->x);
+    g->y = (unsigned)std::min(nj, 65535);
+    g->z = (unsigned)std::max(1, std::min(nk, std::max(1, 148 * 16 / (int)(g->x * g->y))));
+    g->z = std::min<unsigned>(g->z, 65535);
 }
 
 }  // namespace
@@ -66,21 +78,27 @@ unsigned grid_for(long long n) {
 template <class T>
 cudaError_t launch_pack(const FVT<T> &src, const Box &b, T *buf, cudaStream_t s, int *launches) {
     if (box_volume(b) <= 0) return cudaSuccess;
-    pack_kernel<<<grid_for(box_volume(b)), 256, 0, s>>>(src, b, buf);
+    dim3 g, t;
+    grid_for(b, &g, &t);
+    pack_kernel<<<g, t, 0, s>>>(src, b, buf);
     ++*launches;
     return cudaGetLastError();
 }
 template <class T>
 cudaError_t launch_unpack(const T *buf, const Box &b, const FOT<T> &dst, cudaStream_t s, int *launches) {
     if (box_volume(b) <= 0) return cudaSuccess;
-    unpack_kernel<<<grid_for(box_volume(b)), 256, 0, s>>>(buf, b, dst);
+    dim3 g, t;
+    grid_for(b, &g, &t);
+    unpack_kernel<<<g, t, 0, s>>>(buf, b, dst);
     ++*launches;
     return cudaGetLastError();
 }
 template <class T>
 cudaError_t launch_box_copy(const FVT<T> &src, const FOT<T> &dst, const Box &b, cudaStream_t s, int *launches) {
     if (box_volume(b) <= 0) return cudaSuccess;
-    box_copy_kernel<<<grid_for(box_volume(b)), 256, 0, s>>>(src, dst, b);
+    dim3 g, t;
+    grid_for(b, &g, &t);
+    box_copy_kernel<<<g, t, 0, s>>>(src, dst, b);
     ++*launches;
     return cudaGetLastError();
 }
@@ -180,14 +198,6 @@ bool load_nccl() {
     return g_nccl.ok;
 }
 
-// staging for packed messages
-struct Stage {
-    std::mutex mu;
-    void *p = nullptr;
-    size_t n = 0;  // bytes
-};
-Stage g_hstage;
-
 bool is_kinv(const oec_field *f) { return f->stride[2] == 0 && f->ub[2] - f->lb[2] == 1 && f->lb[2] == 0; }
 
 template <class T>
@@ -229,6 +239,82 @@ oec_status check_widths(const int32_t *wlo, const int32_t *whi) {
     return OEC_OK;
 }
 
+// One (message, field) buffer of a rank.  DIRECT: with a j-slab decomposition (px == 1) and a
+// field whose j rows are the slowest dimension (the default i,k,j order, or a k-invariant
+// field), the message's box -- whole j rows, all k, the i range including the i-halo -- lies in
+// ONE contiguous span of the field: it is sent from / received into the field itself (no pack,
+// no kernel).  The span also covers the row padding and any i-halo cells beyond the exchanged
+// width in those rows; with px == 1 those are the global outer halo of the same global rows,
+// which the sender holds as caller data, so the receiver gets the values it would hold anyway.
+// All ranks must pass fields with the same i / k allocation and strides (oec_field_create gives
+// that for equal i / k extents and halos), so both sides compute the same span length.
+// STAGED: other boxes are packed into (unpacked from) a stream-ordered staging buffer.
+template <class T>
+struct MsgBuf {
+    oec_halo_msg m;
+    int field;
+    Box box;       // the field-local box
+    bool direct;
+    size_t count;  // elements on the wire
+    size_t off;    // STAGED: element offset in the rank's staging buffer
+    T *ptr;        // DIRECT: first element of the span; STAGED: set once staging is allocated
+};
+
+template <class T>
+bool span_of(const oec_field *f, const FVT<T> &v, const Box &b, int px, T **p, size_t *count) {
+    if (px != 1) return false;
+    const bool kinv = is_kinv(f);
+    const int64_t ni = f->ub[0] - f->lb[0], nk = f->ub[2] - f->lb[2];
+    const int64_t sj = f->stride[1], sk = kinv ? 0 : f->stride[2];
+    const bool rows_slowest = kinv ? sj >= ni : (sk >= ni && sj >= sk * nk);
+    if (!rows_slowest || b.hi[0] <= b.lo[0] || b.hi[1] <= b.lo[1] || b.hi[2] <= b.lo[2]) return false;
+    const int64_t first = b.lo[0] + (int64_t)b.lo[1] * sj + (int64_t)b.lo[2] * sk;
+    const int64_t last = (b.hi[0] - 1) + (int64_t)(b.hi[1] - 1) * sj + (int64_t)(b.hi[2] - 1) * sk;
+    *p = (T *)v.p + first;
+    *count = (size_t)(last - first + 1);
+    return true;
+}
+
+// the buffers of one rank's plan for n fields; *staged = elements of staging it needs
+template <class T>
+oec_status rank_buffers(const std::vector<oec_halo_msg> &plan, oec_field *const *fields, int32_t n, const int64_t org[3],
+                        int px, std::vector<MsgBuf<T>> *out, size_t *staged) {
+    out->clear();
+    *staged = 0;
+    for (size_t q = 0; q < plan.size(); ++q)
+        for (int f = 0; f < n; ++f) {
+            MsgBuf<T> mb;
+            mb.m = plan[q];
+            mb.field = f;
+            FVT<T> v;
+            oec_status st = view_of(fields[f], &v);
+            if (st || (st = field_box(fields[f], plan[q], org, &mb.box))) return st;
+            mb.direct = span_of(fields[f], v, mb.box, px, &mb.ptr, &mb.count);
+            if (!mb.direct) {
+                mb.count = (size_t)box_volume(mb.box);
+                mb.off = *staged;
+                mb.ptr = nullptr;
+                *staged += mb.count;
+            }
+            out->push_back(mb);
+        }
+    return OEC_OK;
+}
+
+template <class T>
+cudaError_t pack_phase(std::vector<MsgBuf<T>> &bufs, oec_field *const *fields, int phase, bool send, cudaStream_t s,
+                       int *launches) {
+    for (auto &mb : bufs) {
+        if (mb.m.phase != phase || mb.direct || (mb.m.is_send != 0) != send) continue;
+        FVT<T> v;
+        view_of(fields[mb.field], &v);
+        cudaError_t e = send ? launch_pack(v, mb.box, mb.ptr, s, launches)
+                             : launch_unpack((const T *)mb.ptr, mb.box, FOT<T>{(T *)v.p, v.sj, v.sk}, s, launches);
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+}
+
 }  // namespace
 
 template <class T>
@@ -241,68 +327,54 @@ oec_status halo_exchange_impl(oec_decomp *d, oec_field *const *fields, int32_t n
     if (plan.empty() || n == 0) return OEC_OK;
     if (!d->comm) return set_error(OEC_ERR_NCCL, "oec_halo_exchange: decomposition has no NCCL communicator");
     if (!load_nccl()) return set_error(OEC_ERR_NCCL, "oec_halo_exchange: libnccl.so.2 not loadable in this process");
+    for (int f = 0; f < n; ++f)
+        if (!fields[f] || fields[f]->device < 0) return set_error(OEC_ERR_ARG, "oec_halo_exchange: fields must be device memory");
     cudaStream_t s = (cudaStream_t)stream;
-    // staging: one slot per (message, field)
-    std::vector<Box> boxes(plan.size() * n);
-    std::vector<FVT<T>> views(n);
-    size_t total = 0;
-    for (int f = 0; f < n; ++f) {
-        if (fields[f]->device < 0) return set_error(OEC_ERR_ARG, "oec_halo_exchange: fields must be device memory");
-        if ((st = view_of(fields[f], &views[f]))) return st;
-        for (size_t q = 0; q < plan.size(); ++q) {
-            if ((st = field_box(fields[f], plan[q], d->lo, &boxes[q * n + f]))) return st;
-            total += (size_t)box_volume(boxes[q * n + f]);
-        }
-    }
-    std::lock_guard<std::mutex> lock(g_hstage.mu);
-    if (g_hstage.n < total * sizeof(T)) {
-        if (g_hstage.p) cudaFree(g_hstage.p);
-        g_hstage.p = nullptr;
-        g_hstage.n = 0;
-        cudaError_t e = cudaMalloc(&g_hstage.p, total * sizeof(T));
+    std::vector<MsgBuf<T>> bufs;
+    size_t staged = 0;
+    if ((st = rank_buffers(plan, fields, n, d->lo, d->px, &bufs, &staged))) return st;
+    // staging: stream-ordered (allocated and freed on the caller's stream): concurrent exchanges on
+    // other streams and CUDA graphs (graph memory nodes) each get their own; on the fields' device
+    T *stage = nullptr;
+    if (staged) {
+        cudaError_t e = cudaMallocAsync((void **)&stage, staged * sizeof(T), s);
         if (e != cudaSuccess) return set_error(OEC_ERR_CUDA, "halo staging: %s", cudaGetErrorString(e));
-        g_hstage.n = total * sizeof(T);
-    }
-    std::vector<T *> bufs(plan.size() * n);
-    size_t off = 0;
-    for (size_t t = 0; t < bufs.size(); ++t) {
-        bufs[t] = (T *)g_hstage.p + off;
-        off += (size_t)box_volume(boxes[t]);
+        for (auto &mb : bufs)
+            if (!mb.direct) mb.ptr = stage + mb.off;
     }
     constexpr int NCCL_DT = sizeof(T) == 8 ? NCCL_FLOAT64 : NCCL_FLOAT32;
     int launches = 0;
-    for (int phase = 0; phase < 2; ++phase) {
-        for (size_t q = 0; q < plan.size(); ++q)
-            if (plan[q].phase == phase && plan[q].is_send)
-                for (int f = 0; f < n; ++f) {
-                    cudaError_t e = launch_pack(views[f], boxes[q * n + f], bufs[q * n + f], s, &launches);
-                    if (e != cudaSuccess) return set_error(OEC_ERR_CUDA, "halo pack: %s", cudaGetErrorString(e));
-                }
+    oec_status result = OEC_OK;
+    for (int phase = 0; phase < 2 && result == OEC_OK; ++phase) {
+        cudaError_t e = pack_phase(bufs, fields, phase, true, s, &launches);
+        if (e != cudaSuccess) {
+            result = set_error(OEC_ERR_CUDA, "halo pack: %s", cudaGetErrorString(e));
+            break;
+        }
         int r = g_nccl.gstart();
-        for (size_t q = 0; q < plan.size() && r == 0; ++q) {
-            if (plan[q].phase != phase) continue;
-            for (int f = 0; f < n && r == 0; ++f) {
-                const size_t cnt = (size_t)box_volume(boxes[q * n + f]);
-                r = plan[q].is_send ? g_nccl.send(bufs[q * n + f], cnt, NCCL_DT, plan[q].peer, d->comm, s)
-                                    : g_nccl.recv(bufs[q * n + f], cnt, NCCL_DT, plan[q].peer, d->comm, s);
-            }
+        for (auto &mb : bufs) {
+            if (r != 0) break;
+            if (mb.m.phase != phase) continue;
+            r = mb.m.is_send ? g_nccl.send(mb.ptr, mb.count, NCCL_DT, mb.m.peer, d->comm, s)
+                             : g_nccl.recv(mb.ptr, mb.count, NCCL_DT, mb.m.peer, d->comm, s);
         }
         int r2 = g_nccl.gend();
-        if (r || r2)
-            return set_error(OEC_ERR_NCCL, "oec_halo_exchange: NCCL error %d (%s)", r ? r : r2,
-                             g_nccl.errstr ? g_nccl.errstr(r ? r : r2) : "?");
-        for (size_t q = 0; q < plan.size(); ++q)
-            if (plan[q].phase == phase && !plan[q].is_send)
-                for (int f = 0; f < n; ++f) {
-                    FOT<T> o{(T *)views[f].p, views[f].sj, views[f].sk};
-                    cudaError_t e = launch_unpack(bufs[q * n + f], boxes[q * n + f], o, s, &launches);
-                    if (e != cudaSuccess) return set_error(OEC_ERR_CUDA, "halo unpack: %s", cudaGetErrorString(e));
-                }
+        if (r || r2) {
+            result = set_error(OEC_ERR_NCCL, "oec_halo_exchange: NCCL error %d (%s)", r ? r : r2,
+                               g_nccl.errstr ? g_nccl.errstr(r ? r : r2) : "?");
+            break;
+        }
+        if ((e = pack_phase(bufs, fields, phase, false, s, &launches)) != cudaSuccess)
+            result = set_error(OEC_ERR_CUDA, "halo unpack: %s", cudaGetErrorString(e));
     }
-    set_launch_count(launches);
-    return OEC_OK;
+    if (stage) cudaFreeAsync(stage, s);
+    if (result == OEC_OK) set_launch_count(launches);
+    return result;
 }
 
+// The same plans, buffers, pack / unpack kernels and direct spans on ONE device: the transport is
+// a device-to-device copy from the sender's buffer (its staging or its field span) into the
+// receiver's, in place of ncclSend / ncclRecv.  Tests the whole exchange but the NCCL calls.
 template <class T>
 oec_status halo_exchange_local_impl(const int64_t global_domain[3], int32_t px, int32_t py, oec_field *const *fields,
                                     int32_t n, const int32_t width_lo[3], const int32_t width_hi[3], void *stream) {
@@ -310,34 +382,52 @@ oec_status halo_exchange_local_impl(const int64_t global_domain[3], int32_t px, 
     if (st) return st;
     cudaStream_t s = (cudaStream_t)stream;
     const int R = px * py;
-    int launches = 0;
-    for (int phase = 0; phase < 2; ++phase) {
-        for (int r = 0; r < R; ++r) {
-            auto plan = make_plan(global_domain, px, py, r, width_lo, width_hi);
-            for (auto &m : plan) {
-                if (m.phase != phase || m.is_send) continue;
-                for (int f = 0; f < n; ++f) {
-                    const oec_field *src = fields[m.peer * n + f];
-                    oec_field *dst = fields[r * n + f];
-                    int64_t org_d[3], org_s[3], tmp[3];
-                    subdomain(global_domain, px, py, r, org_d, tmp);
-                    subdomain(global_domain, px, py, m.peer, org_s, tmp);
-                    FVT<T> vs, vd;
-                    Box bd, bs;
-                    if ((st = view_of(src, &vs)) || (st = view_of(dst, &vd)) || (st = field_box(dst, m, org_d, &bd)) ||
-                        (st = field_box(src, m, org_s, &bs)))
-                        return st;
-                    // shift the source origin so that the destination's local box indexes it
-                    vs.p += (int64_t)(bs.lo[0] - bd.lo[0]) + (int64_t)(bs.lo[1] - bd.lo[1]) * vs.sj;
-                    FOT<T> o{(T *)vd.p, vd.sj, vd.sk};
-                    cudaError_t e = launch_box_copy(vs, o, bd, s, &launches);
-                    if (e != cudaSuccess) return set_error(OEC_ERR_CUDA, "halo copy: %s", cudaGetErrorString(e));
-                }
-            }
-        }
+    std::vector<std::vector<MsgBuf<T>>> bufs(R);
+    std::vector<size_t> staged(R);
+    size_t total = 0;
+    for (int r = 0; r < R; ++r) {
+        int64_t org[3], tmp[3];
+        subdomain(global_domain, px, py, r, org, tmp);
+        auto plan = make_plan(global_domain, px, py, r, width_lo, width_hi);
+        if ((st = rank_buffers(plan, fields + (size_t)r * n, n, org, px, &bufs[r], &staged[r]))) return st;
+        total += staged[r];
     }
-    set_launch_count(launches);
-    return OEC_OK;
+    T *stage = nullptr;
+    if (total) {
+        cudaError_t e = cudaMallocAsync((void **)&stage, total * sizeof(T), s);
+        if (e != cudaSuccess) return set_error(OEC_ERR_CUDA, "halo staging: %s", cudaGetErrorString(e));
+    }
+    size_t base = 0;
+    for (int r = 0; r < R; ++r) {
+        for (auto &mb : bufs[r])
+            if (!mb.direct) mb.ptr = stage + base + mb.off;
+        base += staged[r];
+    }
+    int launches = 0;
+    oec_status result = OEC_OK;
+    for (int phase = 0; phase < 2 && result == OEC_OK; ++phase) {
+        cudaError_t e = cudaSuccess;
+        for (int r = 0; r < R && e == cudaSuccess; ++r) e = pack_phase(bufs[r], fields + (size_t)r * n, phase, true, s, &launches);
+        for (int r = 0; r < R && e == cudaSuccess && result == OEC_OK; ++r)
+            for (auto &rv : bufs[r]) {
+                if (rv.m.phase != phase || rv.m.is_send) continue;
+                const MsgBuf<T> *sd = nullptr;  // the peer's matching send: same phase, tag and field
+                for (auto &x : bufs[rv.m.peer])
+                    if (x.m.is_send && x.m.peer == r && x.m.phase == phase && x.m.tag == rv.m.tag && x.field == rv.field) sd = &x;
+                if (!sd || sd->count != rv.count) {
+                    result = set_error(OEC_ERR_SHAPE, "oec_halo_exchange_local: rank %d's message from %d does not match "
+                                       "the sender's (%zu vs %zu elements)", r, rv.m.peer, rv.count, sd ? sd->count : 0);
+                    break;
+                }
+                e = cudaMemcpyAsync(rv.ptr, sd->ptr, rv.count * sizeof(T), cudaMemcpyDeviceToDevice, s);
+                if (e != cudaSuccess) break;
+            }
+        for (int r = 0; r < R && e == cudaSuccess; ++r) e = pack_phase(bufs[r], fields + (size_t)r * n, phase, false, s, &launches);
+        if (e != cudaSuccess && result == OEC_OK) result = set_error(OEC_ERR_CUDA, "halo copy: %s", cudaGetErrorString(e));
+    }
+    if (stage) cudaFreeAsync(stage, s);
+    if (result == OEC_OK) set_launch_count(launches);
+    return result;
 }
 
 }  // namespace oec

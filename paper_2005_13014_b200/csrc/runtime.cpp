@@ -284,6 +284,31 @@ struct Staging {
 };
 static Staging g_stage;
 
+// the staging buffers, copy streams and events belong to one device: when the calling thread's
+// current device changes, release them (on their device) and start over on the new one
+static void stage_bind_device() {
+    int cur = 0;
+    cudaGetDevice(&cur);
+    if (g_stage.device == cur) return;
+    if (g_stage.device >= 0) {
+        int keep = cur;
+        cudaSetDevice(g_stage.device);
+        for (void *b : g_stage.bufs)
+            if (b) cudaFree(b);
+        if (g_stage.h2d) {
+            cudaStreamDestroy(g_stage.h2d);
+            cudaStreamDestroy(g_stage.d2h);
+            for (auto &e : g_stage.ev) cudaEventDestroy(e);
+        }
+        cudaSetDevice(keep);
+    }
+    g_stage.bufs.clear();
+    g_stage.sizes.clear();
+    g_stage.h2d = g_stage.d2h = nullptr;
+    for (auto &e : g_stage.ev) e = nullptr;
+    g_stage.device = cur;
+}
+
 static oec_status stage_buffer(size_t idx, size_t bytes, void **p) {
     if (g_stage.bufs.size() <= idx) {
         g_stage.bufs.resize(idx + 1, nullptr);
@@ -567,6 +592,7 @@ static oec_status apply(const ProgDesc &P, const oec_field *const *in, int n_in,
     // s-1 (a third stream) overlap -- PCIe is full duplex.  Each input row is copied once, in the
     // first slab that needs it; the call returns when the outputs are back in host memory.
     std::lock_guard<std::mutex> lock(g_stage.mu);
+    stage_bind_device();  // the device twins live on the caller's current device
     std::vector<oec_field> din(P_n_in), dout(P_n_out);
     std::vector<const oec_field *> pin(P_n_in);
     std::vector<oec_field *> pout(P_n_out);
@@ -577,7 +603,7 @@ static oec_status apply(const ProgDesc &P, const oec_field *const *in, int n_in,
         void *dptr;
         if ((st = stage_buffer(slot++, b1 - b0, &dptr))) return st;
         din[q] = *in[q];
-        din[q].device = 0;
+        din[q].device = g_stage.device;
         din[q].data = (char *)dptr + ((uintptr_t)in[q]->data - b0);
         pin[q] = &din[q];
         total += b1 - b0;
@@ -588,7 +614,7 @@ static oec_status apply(const ProgDesc &P, const oec_field *const *in, int n_in,
         void *dptr;
         if ((st = stage_buffer(slot++, b1 - b0, &dptr))) return st;
         dout[q] = *out[q];
-        dout[q].device = 0;
+        dout[q].device = g_stage.device;
         dout[q].data = (char *)dptr + ((uintptr_t)out[q]->data - b0);
         pout[q] = &dout[q];
     }
@@ -792,6 +818,10 @@ oec_status oec_program_input(const char *program, int32_t idx, const char **name
     }
     if (k_invariant) *k_invariant = P->in_kinv[idx];
     return OEC_OK;
+}
+
+oec_status oec_program_extent(const char *program, int32_t input_idx, int64_t lo[3], int64_t hi[3]) {
+    return oec_program_input(program, input_idx, nullptr, lo, hi, nullptr);
 }
 
 oec_status oec_program_output(const char *program, int32_t idx, const char **name) {

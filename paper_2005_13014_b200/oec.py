@@ -84,6 +84,7 @@ SIGNATURES = {
     "oec_program_info": (C.c_int, [C.c_char_p, C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
     "oec_program_input": (C.c_int, [C.c_char_p, C.c_int32, C.POINTER(C.c_char_p), C.POINTER(C.c_int64),
                                     C.POINTER(C.c_int64), C.POINTER(C.c_int32)]),
+    "oec_program_extent": (C.c_int, [C.c_char_p, C.c_int32, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     "oec_program_output": (C.c_int, [C.c_char_p, C.c_int32, C.POINTER(C.c_char_p)]),
     "oec_program_scalar": (C.c_int, [C.c_char_p, C.c_int32, C.POINTER(C.c_char_p), C.POINTER(C.c_double)]),
     "oec_hdiff": (C.c_int, [_P, _P, _P, C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.c_void_p]),
@@ -341,6 +342,13 @@ def oec_program_input(program: str, idx: int):
     kinv = C.c_int32()
     _check(lib().oec_program_input(program.encode(), idx, C.byref(name), lo, hi, C.byref(kinv)))
     return name.value.decode(), tuple(lo), tuple(hi), bool(kinv.value)
+
+
+def oec_program_extent(program: str, idx: int):
+    """(lo, hi): the access extent of input idx relative to the domain."""
+    lo, hi = I64x3(), I64x3()
+    _check(lib().oec_program_extent(program.encode(), idx, lo, hi))
+    return tuple(lo), tuple(hi)
 
 
 def oec_program_output(program: str, idx: int) -> str:

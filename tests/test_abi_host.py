@@ -56,6 +56,8 @@ def test_registry_matches_recipe_and_trace(program):
         assert kinv == s.k_invariant
     for (name, dflt), (sname, sval) in zip(scs, spec.scalars):
         assert dflt == sval
+    for q, (name, lo, hi, kinv) in enumerate(ins):  # oec_program_extent == oec_program_input
+        assert oec.oec_program_extent(program, q) == (lo, hi)
     if program == "vadv":
         return  # vadv's extent is pinned by the oracle's range checks (test_oracle_vadv)
     # brute-force trace of the fused oracle evaluation on a small domain

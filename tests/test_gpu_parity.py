@@ -276,3 +276,67 @@ def test_hdiff_large_config_ragged():
     _check("hdiff", (517, 1000, 17), seed=7, order=(0, 1, 2))
     # just below the threshold: the small-tile configuration on a multi-million-point domain
     _check("hdiff", (1031, 1029, 3), seed=8)
+
+
+# ---- vadv launch modes (csrc/vadv.cu): single wave, persistent multi-block, 2D grid ----
+@pytest.mark.parametrize("order", ORDERS)
+@pytest.mark.parametrize("domain", [
+    (128, 128, 80),   # one wave of 128 one-row blocks
+    (120, 130, 80),   # ragged rows (120 of 128 columns live)
+    (100, 150, 41),   # 150 blocks on 148 SMs: persistent, two CTAs walk two blocks; K not a multiple of 8
+    (16, 1184, 12),   # 1184 narrow blocks (16 live columns each), persistent
+    (128, 128, 84),   # the tallest column of the TMEM solver
+])
+def test_vadv_single_wave_and_narrow_blocks(domain, order):
+    _check("vadv", domain, seed=11, order=order)
+
+
+def test_vadv_subdomain_offset():
+    # a sub-domain call (dom_lb, dom_ub not at the allocation origin)
+    _check("vadv", (128, 96, 20), seed=12, dom_lb=(16, 3, 2), dom_ub=(128, 95, 19), out_halo=(0, 0, 0))
+
+
+def _check_sampled(program, domain, boxes, seed=0):
+    host = synth.make_inputs(program, domain, seed=seed)
+    g = run_gpu(program, host, domain)
+    for lo, hi in boxes:
+        r = run_oracle(program, host, domain, dom_lb=lo, dom_ub=hi)
+        for name in synth.PROGRAMS[program].outputs:
+            _assert_parity(domain_part(g[name], lo, hi), r[name], (program, name, domain, lo, hi))
+
+
+def test_vadv_persistent_full_compare_paper_size():
+    # 256x256x60 (the paper's large size): 512 column blocks on <= 148 persistent CTAs --
+    # every CTA walks 3-4 blocks, carrying its ring, mbarrier phases and TMEM across them
+    _check("vadv", (256, 256, 60), seed=13)
+
+
+@pytest.mark.parametrize("domain", [(384, 384, 80), (512, 512, 80)])
+def test_vadv_persistent_sampled(domain):
+    # 1152 / 2048 blocks: persistent (<= 12 per CTA) resp. 2D grid; the samples cover blocks that a
+    # persistent CTA reaches first, second and last (block b runs on CTA b % grid as its b / grid-th)
+    ni, nj, nk = domain
+    boxes = [((0, 0, 0), (256, 2, nk)),                       # blocks 0..3: first blocks of CTAs 0..3
+             ((0, 148 // (ni // 128), 0), (ni, 148 // (ni // 128) + 2, nk)),  # second blocks of CTA 0..
+             ((ni - 200, nj - 3, 0), (ni, nj, nk)),           # the last blocks (last trips)
+             ((130, nj // 2, 0), (250, nj // 2 + 1, nk))]
+    _check_sampled("vadv", domain, boxes, seed=14)
+
+
+@pytest.mark.parametrize("program", synth.ALL_PROGRAMS)
+def test_every_program_paper_large_size(program):
+    # 256x256x60 over the whole domain
+    if program == "vadv":
+        pytest.skip("covered by test_vadv_persistent_full_compare_paper_size")
+    _check(program, (256, 256, 60), seed=15)
+
+
+@pytest.mark.parametrize("program", synth.ALL_PROGRAMS)
+def test_every_program_c5_size_sampled(program):
+    # BASELINE.json configs[4]: 512x512x80 per GPU, in the launch configuration bench.py --config c5
+    # times; the oracle on sub-boxes at the corners, edges and centre
+    ni, nj, nk = 512, 512, 80
+    kk = (0, nk) if program == "vadv" else (10, 70)  # a vadv column is solved over its whole k range
+    boxes = [((0, 0, 0), (40, 24, nk)), ((ni - 40, nj - 24, 0), (ni, nj, nk)), ((230, 250, kk[0]), (300, 270, kk[1])),
+             ((0, nj - 10, 0), (ni, nj, nk if program == "vadv" else 3))]
+    _check_sampled(program, (ni, nj, nk), boxes, seed=16)

@@ -1,15 +1,18 @@
 #!/bin/bash
-# full GPU pass: tests, smoke, bench (default), ncu launch list of the bench command, ncu --set full
-# of the hot kernels.  Outputs in gpurun_out/ (scratch); summaries are copied into profiles/.
+# One validation pass on the GPU box: GPU tests, smoke, the default bench (+ reference arm) and the
+# multi-GPU configurations at N=1.  Outputs under gpurun_out/<TAG>_*.
 cd "$GRAFT_REPO_ROOT" || exit 1
+TAG=${TAG:-r02}
 mkdir -p gpurun_out
-TAG=${1:-r01}
-timeout 1200 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu_$TAG.txt 2>&1; echo "pytest exit $?" >> gpurun_out/pytest_gpu_$TAG.txt
-timeout 300 python __graft_entry__.py --smoke > gpurun_out/smoke_$TAG.txt 2>&1; echo "smoke exit $?" >> gpurun_out/smoke_$TAG.txt
-timeout 600 python bench.py > gpurun_out/bench_$TAG.json 2> gpurun_out/bench_$TAG.err
-timeout 600 python bench.py --impl reference --steps 20 --warmup 3 > gpurun_out/bench_ref_$TAG.json 2> gpurun_out/bench_ref_$TAG.err
-timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:"hdiff_|vadv_" -c 60 --csv --log-file gpurun_out/launches_$TAG.csv python bench.py --steps 14 --warmup 3 --e2e-steps 0 --no-suite --no-cpu --sets 7 > gpurun_out/ncu_bench_$TAG.log 2>&1
-for p in hdiff vadv; do
-  timeout 300 ncu --set full --clock-control none --import-source on -k regex:"${p}_(tma|sp)" -s 2 -c 1 -o gpurun_out/prof_${p}_$TAG -f python tools/kernel_driver.py --program $p --reps 4 > gpurun_out/ncu_${p}_$TAG.log 2>&1
+if [ -z "$NO_TESTS" ]; then
+  timeout 2400 python -m pytest tests -m gpu -q -x > gpurun_out/${TAG}_pytest_gpu.txt 2>&1; echo "pytest rc=$?" >> gpurun_out/${TAG}_pytest_gpu.txt
+  timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${TAG}_smoke.txt 2>&1; echo "smoke rc=$?" >> gpurun_out/${TAG}_smoke.txt
+fi
+timeout 900 python bench.py --detail gpurun_out/${TAG}_bench_detail.json > gpurun_out/${TAG}_bench.json 2> gpurun_out/${TAG}_bench.err; echo "bench rc=$?" >> gpurun_out/${TAG}_bench.err
+timeout 600 python bench.py --impl reference --steps 20 --warmup 5 > gpurun_out/${TAG}_bench_ref.json 2>&1
+for c in ${CONFIGS:-c3 c4 c5}; do
+  timeout 900 python bench.py --config $c --no-extras --no-cpu --detail gpurun_out/${TAG}_bench_${c}_detail.json > gpurun_out/${TAG}_bench_${c}.json 2> gpurun_out/${TAG}_bench_${c}.err; echo "rc=$?" >> gpurun_out/${TAG}_bench_${c}.err
 done
-echo done
+tail -3 gpurun_out/${TAG}_pytest_gpu.txt 2>/dev/null; tail -2 gpurun_out/${TAG}_smoke.txt 2>/dev/null
+tail -c 2500 gpurun_out/${TAG}_bench.json; tail -3 gpurun_out/${TAG}_bench.err
+for c in ${CONFIGS:-c3 c4 c5}; do tail -c 1500 gpurun_out/${TAG}_bench_${c}.json; tail -2 gpurun_out/${TAG}_bench_${c}.err; done

@@ -33,10 +33,11 @@ def main():
         for r in range(8):
             oec.oec_apply_program("vadv", sets[r][0], sets[r][1], [0.15], (0, 0, 0), dom)
         torch.cuda.synchronize()
-    ncta = min(1024, ((dom[0] + 127) // 128) * dom[1])
     buf = (C.c_ulonglong * (4 * 1024))()
     oec.lib().oec_debug_vadv_cta(buf)
-    t = np.array(buf[:], dtype=np.int64).reshape(4, 1024)[:, :ncta]
+    t = np.array(buf[:], dtype=np.int64).reshape(4, 1024)
+    ncta = int(np.count_nonzero(t[0]))  # CTAs that ran (any launch mode)
+    t = t[:, :ncta]
     t0 = t[0].min()
     names = ["start", "first chunk", "forward done", "end"]
     print(f"domain {dom}, {ncta} CTAs; times in us after the earliest CTA start")
@@ -46,6 +47,16 @@ def main():
     fwd = (t[2] - t[1]) / 1e3
     bwd = (t[3] - t[2]) / 1e3
     print(f"forward (first chunk -> done) med {np.median(fwd):.2f} us, backward med {np.median(bwd):.2f} us")
+    tr = (C.c_ulonglong * (8 * 256))()
+    oec.lib().oec_debug_vadv_trace(tr)
+    tt = np.array(tr[:], dtype=np.int64).reshape(8, 256)
+    c1 = tt[1][tt[1] > 0]
+    if len(c1):
+        print("CTA 0 chunk arrivals (us after its start):", np.round((np.sort(c1) - t[0][0]) / 1e3, 2).tolist()[:24])
+    for role, name in ((4, "chain groups done"), (5, "rows groups done")):
+        c = tt[role][tt[role] > 0]
+        if len(c):
+            print(f"CTA 0 {name} (us):", np.round((np.sort(c) - t[0][0]) / 1e3, 2).tolist()[:24])
 
 
 if __name__ == "__main__":
