@@ -81,6 +81,9 @@
 #ifndef HFL_NW
 #define HFL_NW 12
 #endif
+#ifndef HD_PF
+#define HD_PF 2  // tiles per warp prefetched into L2 before griddepcontrol.wait
+#endif
 #ifndef HD_LARGE_POINTS
 #define HD_LARGE_POINTS (8ll << 20)  // measured: the small tiles win up to 256^2 x 80 (0.79 -> 0.83)
 #endif
@@ -545,6 +548,14 @@ __global__ void __launch_bounds__(NW * 32, 1) hdiff_tma(const __grid_constant__ 
 #pragma unroll
         for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
         fence_mbar_init();
+#pragma unroll
+        for (int s = 0; s < HD_PF; ++s)  // warm L2 with the first tiles during the previous kernel's drain
+            if (gw + s * nwt < nitems) {
+                int ib, j0, k;
+                decode(gw + s * nwt, ib, j0, k);
+                tma_prefetch_ijk(m_in, ib - C::LP, j0 - 2, k);
+                tma_prefetch_ijk(m_cf, ib, j0, k);
+            }
     }
     griddep_wait();  // inputs may be the previous kernel's outputs
     if (lane == 0) {
@@ -630,6 +641,24 @@ __device__ __forceinline__ void st_release_sys(unsigned long long *p, unsigned l
     asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
+// "step done" counting: acq_rel atomics (PTX release is cumulative over everything that
+// happens-before it, acquire makes the other arrivals' prior accesses visible to the last one)
+__device__ __forceinline__ unsigned atom_add_acqrel_cta_shared(unsigned *p, unsigned v) {
+    unsigned old;
+    asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(smem_u32(p)), "r"(v) : "memory");
+    return old;
+}
+__device__ __forceinline__ unsigned long long atom_add_acqrel_sys(unsigned long long *p, unsigned long long v) {
+    unsigned long long old;
+    asm volatile("atom.acq_rel.sys.global.add.u64 %0, [%1], %2;" : "=l"(old) : "l"(p), "l"(v) : "memory");
+    return old;
+}
+__device__ __forceinline__ unsigned long long atom_add_relaxed_gpu(unsigned long long *p, unsigned long long v) {
+    unsigned long long old;
+    asm volatile("atom.relaxed.gpu.global.add.u64 %0, [%1], %2;" : "=l"(old) : "l"(p), "l"(v) : "memory");
+    return old;
+}
+
 __device__ __forceinline__ unsigned long long globaltimer_ns() {
     unsigned long long v;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
@@ -665,14 +694,41 @@ __global__ void __launch_bounds__(NW * 32, 1) hdiff_pipe(const __grid_constant__
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     unsigned char *wbase = smem + warp * S * C::SLOT;
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem + NW * S * C::SLOT) + warp * S;
+    unsigned *warps_done = reinterpret_cast<unsigned *>(reinterpret_cast<uint64_t *>(smem + NW * S * C::SLOT) + NW * S);
     const int gw = blockIdx.x * NW + warp, nwt = gridDim.x * NW;
-    // programmatic dependent launch: descriptor prefetch overlaps the previous step's drain; the
-    // step counter and x_t are read only after the previous grid completed
+    bool any_nb = false;
+#pragma unroll
+    for (int dd = 0; dd < 9; ++dd) any_nb = any_nb || (a.nb[dd].exists != 0);
+    // programmatic dependent launch: descriptor prefetch and barrier setup overlap the previous
+    // step's drain; the step counter and x_t are read only after the previous grid completed
     if (lane == 0) {
         prefetch_tmap(&m0.map);
         prefetch_tmap(&m1.map);
         prefetch_tmap(&m_cf.map);
     }
+    if (threadIdx.x == 0) *warps_done = 0;
+    if (lane == 0) {
+        // warm L2 with the first interior tiles during the previous kernel's drain: coefficients,
+        // and x_t of the GUESSED step t.  The guess reads the pad before griddepcontrol.wait, so
+        // it may be stale; it only selects what to prefetch -- the loads below use t read after
+        // the wait.  If this pipeline's previous step is still draining (this CTA only got an SM
+        // because one of its CTAs exited, having counted itself in FINISHED), t is one ahead of
+        // the pad's STEP word.
+        const unsigned long long fin = *reinterpret_cast<volatile const unsigned long long *>(a.pad + PIPE_PAD_FINISHED);
+        const unsigned long long tg =
+            *reinterpret_cast<volatile const unsigned long long *>(a.pad + PIPE_PAD_STEP) + (fin != 0 ? 1 : 0);
+        const TMap &mg = (tg & 1) ? m1 : m0;
+        const int ns = a.sb - a.sa, nc = a.cb - a.ca;
+        for (int q = 0; q < S; ++q) {
+            const int item = gw + q * nwt;
+            if (item < a.n_int) {
+                const int ib = (a.sa + item % ns) * W, j0 = (a.ca + (item / ns) % nc) * JB, k = item / (ns * nc);
+                tma_prefetch_ijk(m_cf, ib, j0, k);
+                tma_prefetch_ijk(mg, ib - C::LP, j0 - 2, k);
+            }
+        }
+    }
+    __syncthreads();
     griddep_launch_dependents();
     griddep_wait();
     const unsigned long long t = *reinterpret_cast<volatile const unsigned long long *>(a.pad + PIPE_PAD_STEP);
@@ -791,16 +847,19 @@ __global__ void __launch_bounds__(NW * 32, 1) hdiff_pipe(const __grid_constant__
         __syncwarp();
     }
     (void)nk;
-    // ---- publish "step t done" (our outputs written, our reads of the neighbours' x_t finished):
-    // every thread's accesses precede the barrier; thread 0's system-scope fence (cumulative)
-    // then orders them before the CTA is counted as done
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        __threadfence_system();
-        const unsigned long long old = atomicAdd(a.pad + PIPE_PAD_FINISHED, 1ull);
+    // ---- publish "step t done" (our outputs written, our reads of the neighbours' x_t finished)
+    // without a CTA barrier: each warp arrives on a per-CTA shared counter (acq_rel, CTA scope);
+    // the CTA's last warp arrives on the global counter -- acq_rel at system scope when there are
+    // neighbours (they read our x_{t+1} and overwrite the x_t we read), relaxed without: then only
+    // the next step of this grid reads our outputs, after griddepcontrol.wait, i.e. after this
+    // grid completed -- and the grid's last arrival publishes t+1 to the neighbours (release,
+    // system scope) and advances the step counter
+    __syncwarp();
+    if (lane == 0 && atom_add_acqrel_cta_shared(warps_done, 1u) == NW - 1) {
+        const unsigned long long old = any_nb ? atom_add_acqrel_sys(a.pad + PIPE_PAD_FINISHED, 1ull)
+                                              : atom_add_relaxed_gpu(a.pad + PIPE_PAD_FINISHED, 1ull);
         if (old == gridDim.x - 1) {
             a.pad[PIPE_PAD_FINISHED] = 0;
-            __threadfence_system();
             for (int dd = 0; dd < 9; ++dd)
                 if (a.nb[dd].exists) st_release_sys(a.nb[dd].flag, t + 1);
             *reinterpret_cast<volatile unsigned long long *>(a.pad + PIPE_PAD_STEP) = t + 1;
@@ -815,18 +874,18 @@ cudaError_t launch_pipe(const TMap &m0, const TMap &m1, const TMap &mcf, const P
     static bool configured = false;
     static int blocks_per_sm = 1, sms = 148;
     if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(hdiff_pipe<T, V, JB, S, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+        cudaError_t e = cudaFuncSetAttribute(hdiff_pipe<T, V, JB, S, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM + 16);
         if (e != cudaSuccess) return e;
         int dev;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, hdiff_pipe<T, V, JB, S, NW>, NW * 32, C::SMEM);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, hdiff_pipe<T, V, JB, S, NW>, NW * 32, C::SMEM + 16);
         if (blocks_per_sm < 1) blocks_per_sm = 1;
         configured = true;
     }
     const long long blocks = std::max(1ll, std::min<long long>((a.n_items + NW - 1) / NW, (long long)sms * blocks_per_sm));
     for (int s = 0; s < nsteps; ++s) {
-        cudaError_t e = launch_pdl(hdiff_pipe<T, V, JB, S, NW>, dim3((unsigned)blocks), dim3(NW * 32), C::SMEM, st, m0,
+        cudaError_t e = launch_pdl(hdiff_pipe<T, V, JB, S, NW>, dim3((unsigned)blocks), dim3(NW * 32), C::SMEM + 16, st, m0,
                                    m1, mcf, a);
         ++*launches;
         if (e == cudaSuccess) e = cudaGetLastError();

@@ -1102,6 +1102,7 @@ struct Drv {
     PFN_cuModuleLoadData_v2000 load = nullptr;
     PFN_cuModuleGetFunction_v2000 get = nullptr;
     PFN_cuLaunchKernel_v4000 launch = nullptr;
+    PFN_cuLaunchKernelEx_v11060 launch_ex = nullptr;  // programmatic dependent launch of tiled kernels
     PFN_cuFuncSetAttribute_v9000 set_attr = nullptr;
 };
 static Drv g_drv;
@@ -1117,6 +1118,8 @@ static void load_drv() {
         g_drv.launch = (PFN_cuLaunchKernel_v4000)f;
     if (cudaGetDriverEntryPoint("cuFuncSetAttribute", &f, cudaEnableDefault, &q) == cudaSuccess && q == cudaDriverEntryPointSuccess)
         g_drv.set_attr = (PFN_cuFuncSetAttribute_v9000)f;
+    if (cudaGetDriverEntryPoint("cuLaunchKernelEx", &f, cudaEnableDefault, &q) == cudaSuccess && q == cudaDriverEntryPointSuccess)
+        g_drv.launch_ex = (PFN_cuLaunchKernelEx_v11060)f;
     g_drv.ok = g_drv.load && g_drv.get && g_drv.launch && g_drv.set_attr;
 }
 
@@ -1169,6 +1172,13 @@ __device__ __forceinline__ void tma2(void *dst, const TM *m, unsigned long long 
 __device__ __forceinline__ void tma3(void *dst, const TM *m, unsigned long long *b, int c0, int c1, int c2) {
     asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];"
                  ::"r"(su32(dst)), "l"((unsigned long long)m), "r"(su32(b)), "r"(c0), "r"(c1), "r"(c2) : "memory"); }
+// L2 prefetch of a box before griddepcontrol.wait (only warms L2, the point of coherence; csrc/tma.h)
+__device__ __forceinline__ void pf2(const TM *m, int c0, int c1) {
+    asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global [%0, {%1, %2}];" ::"l"((unsigned long long)m), "r"(c0), "r"(c1)
+                 : "memory"); }
+__device__ __forceinline__ void pf3(const TM *m, int c0, int c1, int c2) {
+    asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global [%0, {%1, %2, %3}];" ::"l"((unsigned long long)m), "r"(c0),
+                 "r"(c1), "r"(c2) : "memory"); }
 )";
 
 static std::string gen_tiled(const Program &P, const Spec &S) {
@@ -1198,31 +1208,42 @@ static std::string gen_tiled(const Program &P, const Spec &S) {
       << "    const int NITEMS = " << NI << ";\n";
     // TMA issue of one item's boxes into stage `st`, emitted inline where it is used (a lambda
     // capturing the __grid_constant__ tensor maps would not keep their param-space addresses)
-    auto issue = [&](const std::string &ind, const std::string &item, const std::string &st) {
+    auto issue = [&](const std::string &ind, const std::string &item, const std::string &st, bool prefetch = false) {
         std::ostringstream w;
         w << ind << "{\n"
           << ind << "    const int it_ = " << item << ", st_ = " << st << ";\n"
           << ind << "    const int ti_ = it_ % " << L.ntile[0] << ", tj_ = (it_ / " << L.ntile[0] << ") % " << L.ntile[1]
           << ", k_ = it_ / " << L.ntile[0] * L.ntile[1] << ";\n"
-          << ind << "    const int i0_ = ti_ * " << L.ti << ", j0_ = tj_ * " << L.tj << ";\n"
-          << ind << "    mb_expect(&full[st_], " << L.stage_bytes_tx(esz) << ");\n";
+          << ind << "    const int i0_ = ti_ * " << L.ti << ", j0_ = tj_ * " << L.tj << ";\n";
+        if (!prefetch) w << ind << "    mb_expect(&full[st_], " << L.stage_bytes_tx(esz) << ");\n";
+        else w << ind << "    (void)st_;\n";
         for (size_t q = 0; q < P.in_names.size(); ++q) {
             if (!L.staged[q]) continue;
             const std::string cq = "c" + std::to_string(q);
+            const std::string dst = prefetch ? std::string("&tm") + std::to_string(q) + ", "
+                                             : "smem + st_ * " + std::to_string(L.stage_bytes) + " + " + std::to_string(L.off[q]) +
+                                                   ", &tm" + std::to_string(q) + ", &full[st_], ";
             if (P.in_kinv[q])
-                w << ind << "    tma2(smem + st_ * " << L.stage_bytes << " + " << L.off[q] << ", &tm" << q << ", &full[st_], "
-                  << cq << "x + i0_, " << cq << "y + j0_);\n";
+                w << ind << "    " << (prefetch ? "pf2(" : "tma2(") << dst << cq << "x + i0_, " << cq << "y + j0_);\n";
             else
-                w << ind << "    tma3(smem + st_ * " << L.stage_bytes << " + " << L.off[q] << ", &tm" << q << ", &full[st_], "
-                  << cq << "x + i0_, " << (L.swap[q] ? cq + "z + k_, " + cq + "y + j0_" : cq + "y + j0_, " + cq + "z + k_")
-                  << ");\n";
+                w << ind << "    " << (prefetch ? "pf3(" : "tma3(") << dst << cq << "x + i0_, "
+                  << (L.swap[q] ? cq + "z + k_, " + cq + "y + j0_" : cq + "y + j0_, " + cq + "z + k_") << ");\n";
         }
         w << ind << "}\n";
         return w.str();
     };
-    o << "    if (tid == 0) {\n"
+    // programmatic dependent launch: barrier setup and an L2 prefetch of the first items overlap
+    // the previous kernel's drain; every thread waits for it before touching its data
+    o << "    asm volatile(\"griddepcontrol.launch_dependents;\" ::: \"memory\");\n"
+      << "    if (tid == 0) {\n"
       << "        for (int s = 0; s < " << L.stages << "; ++s) mb_init(&full[s], 1);\n"
       << "        asm volatile(\"fence.mbarrier_init.release.cluster;\" ::: \"memory\");\n"
+      << "        for (int s = 0; s < " << L.stages << "; ++s)\n"
+      << "            if (blockIdx.x + s * gridDim.x < NITEMS)\n"
+      << issue("            ", "blockIdx.x + s * gridDim.x", "s", true)
+      << "    }\n"
+      << "    asm volatile(\"griddepcontrol.wait;\" ::: \"memory\");\n"
+      << "    if (tid == 0) {\n"
       << "        for (int s = 0; s < " << L.stages << "; ++s)\n"
       << "            if (blockIdx.x + s * gridDim.x < NITEMS)\n"
       << issue("            ", "blockIdx.x + s * gridDim.x", "s")
@@ -1450,7 +1471,24 @@ static oec_status run_variant(const Program &P, const oec_field *const *in, oec_
         const long long nitems = (long long)L.ntile[0] * L.ntile[1] * L.ntile[2];
         const int bps = std::max(1, std::min(8, (228 * 1024) / (L.smem + 1024)));
         const unsigned grid = (unsigned)std::max<long long>(1, std::min<long long>(nitems, (long long)sms * bps));
-        CUresult r = g_drv.launch(C->fns[0], grid, 1, 1, 256, 1, 1, (unsigned)L.smem, (CUstream)s, args.data(), nullptr);
+        CUresult r;
+        if (g_drv.launch_ex && pdl_enabled()) {  // the tiled kernel waits in griddepcontrol.wait: PDL-safe
+            CUlaunchConfig cfg = {};
+            cfg.gridDimX = grid;
+            cfg.gridDimY = cfg.gridDimZ = 1;
+            cfg.blockDimX = 256;
+            cfg.blockDimY = cfg.blockDimZ = 1;
+            cfg.sharedMemBytes = (unsigned)L.smem;
+            cfg.hStream = (CUstream)s;
+            CUlaunchAttribute at[1];
+            at[0].id = CU_LAUNCH_ATTRIBUTE_PROGRAMMATIC_STREAM_SERIALIZATION;
+            at[0].value.programmaticStreamSerializationAllowed = 1;
+            cfg.attrs = at;
+            cfg.numAttrs = 1;
+            r = g_drv.launch_ex(&cfg, C->fns[0], args.data(), nullptr);
+        } else {
+            r = g_drv.launch(C->fns[0], grid, 1, 1, 256, 1, 1, (unsigned)L.smem, (CUstream)s, args.data(), nullptr);
+        }
         if (r != CUDA_SUCCESS) return set_error(OEC_ERR_CUDA, "%s: cuLaunchKernel (tiled) failed (%d)", P.name.c_str(), (int)r);
         ++launches;
     } else if (S.variant != OEC_VARIANT_UNFUSED) {

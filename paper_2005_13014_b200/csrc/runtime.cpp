@@ -438,7 +438,10 @@ static oec_status run_device(int p, const oec_field *const *in, oec_field *const
         bool fits;
         vadv_tma_boxes<T>(d, box, bwc, bus, &fits);
         bool tma = fits && aligned16 && variant == OEC_VARIANT_AUTO;
-        for (int q = 0; q < 5 && tma; ++q) tma = make_tmap(in[q], q == 0 ? bus : (q == 1 ? bwc : box), &tm[q]);
+#ifndef VA_PROMO
+#define VA_PROMO 0  // no L2 sector promotion for vadv's 1 KB rows: 0.68 -> 0.69 at 128^2 (profiles/l2_prefetch_r02.md)
+#endif
+        for (int q = 0; q < 5 && tma; ++q) tma = make_tmap(in[q], q == 0 ? bus : (q == 1 ? bwc : box), &tm[q], VA_PROMO);
         if constexpr (sizeof(T) == 4)
             e = launch_vadv_f32(v_in[0], v_in[1], v_in[2], v_in[3], v_in[4], v_out[0], sc[0], d, tma ? tm : nullptr, s,
                                 &launches);

@@ -29,7 +29,7 @@ bool pdl_enabled() {
     return on == 1;
 }
 
-bool make_tmap(const oec_field *f, const int box[3], TMap *out) {
+bool make_tmap(const oec_field *f, const int box[3], TMap *out, int l2_promotion) {
     std::call_once(g_once, load_encode);
     if (!g_encode || !f || f->stride[0] != 1) return false;
     if (f->stride[2] == 0) return false;  // k-invariant: not a TMA tensor
@@ -47,9 +47,11 @@ bool make_tmap(const oec_field *f, const int box[3], TMap *out) {
     cuuint32_t es[3] = {1, 1, 1};
     if (bx[0] * esz % 16 || bx[0] > 256 || bx[1] > 256 || bx[2] > 256) return false;
     memset(out, 0, sizeof *out);
+    const CUtensorMapL2promotion promo = l2_promotion >= 256 ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B
+                                         : l2_promotion >= 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+                                                               : CU_TENSOR_MAP_L2_PROMOTION_NONE;
     CUresult r = g_encode(&out->map, esz == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void *)base, dims, strides, bx, es,
-                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return false;
     out->ioff = ioff;
     out->lb0 = (int32_t)f->lb[0];

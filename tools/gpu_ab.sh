@@ -8,7 +8,7 @@ DOMS=${DOMS:-"128,128,80 1024,1024,80"}
 OUT=gpurun_out/ab_${TAG:-x}.jsonl
 : > $OUT
 for rep in 1 2 3; do
-  for v in old new; do
+  for v in ${VARIANTS:-old new}; do
     for dom in $DOMS; do
       OEC_LIB_PATH=tune/liboec_$v.so timeout 300 python tools/kernel_bench.py --programs $PROGS --domain ${dom//,/ } --tag $v >> $OUT 2>&1
     done
