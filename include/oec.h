@@ -325,8 +325,10 @@ oec_status oec_decomp_plan(const oec_decomp *d, const int32_t width_lo[3], const
  * groups over NVLink/NVSwitch), enqueued on `stream`.  Each field is described in the rank's
  * LOCAL coordinates (origin = the rank's sub-domain lower bound local_lb, exactly like a
  * single-GPU field of that sub-domain) and must cover the sub-domain grown by the widths.
- * Boxes are packed/unpacked by liboec kernels around the NCCL calls.  Errors: OEC_ERR_NCCL when
- * no communicator / NCCL unavailable, OEC_ERR_SHAPE when a field does not cover the halo. */
+ * Boxes are packed/unpacked by liboec kernels around the NCCL calls (j-slab rows, px == 1, are
+ * sent from / received into the field itself).  Errors: OEC_ERR_NCCL when no communicator /
+ * NCCL unavailable, OEC_ERR_SHAPE when a field does not cover the halo or a width exceeds a
+ * neighbour's sub-domain (two hops would be needed). */
 oec_status oec_halo_exchange(oec_decomp *d, oec_field *const *fields, int32_t n, const int32_t width_lo[3],
                              const int32_t width_hi[3], void *stream);
 
@@ -336,6 +338,21 @@ oec_status oec_halo_exchange(oec_decomp *d, oec_field *const *fields, int32_t n,
  * Used to test decomposition logic on a single GPU. */
 oec_status oec_halo_exchange_local(const int64_t global_domain[3], int32_t px, int32_t py, oec_field *const *fields,
                                    int32_t n, const int32_t width_lo[3], const int32_t width_hi[3], void *stream);
+
+/* As oec_halo_exchange_local on a global domain that is periodic in i (periodic[0] != 0) and/or
+ * j (periodic[1] != 0); periodic may be NULL (= neither). */
+oec_status oec_halo_exchange_local_periodic(const int64_t global_domain[3], int32_t px, int32_t py,
+                                            const int32_t periodic[2], oec_field *const *fields, int32_t n,
+                                            const int32_t width_lo[3], const int32_t width_hi[3], void *stream);
+
+/* Make the global domain of d periodic in i and/or j (default: neither; not in PAPER.md -- a
+ * global latitude-longitude grid wraps in i).  The first and last rank of a rank-grid row
+ * (column) become neighbours -- with px == 1 (py == 1) the rank exchanges with ITSELF, which is
+ * how the NCCL transport is exercised on one GPU.  Receive boxes then lie outside [0, global
+ * domain) in the receiver's frame (oec_decomp_plan) and equal the sender's box modulo the
+ * period.  NCCL pairs a rank's messages to one peer in issue order: oec_halo_exchange issues
+ * them by (peer, tag, field) on both sides.  Errors: OEC_ERR_ARG (NULL d). */
+oec_status oec_decomp_set_periodic(oec_decomp *d, int32_t periodic_i, int32_t periodic_j);
 
 oec_status oec_decomp_destroy(oec_decomp *d);
 

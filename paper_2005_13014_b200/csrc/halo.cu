@@ -21,6 +21,7 @@ struct oec_decomp {
     int32_t px, py, rank, ri, rj;
     int64_t lo[3], hi[3];
     void *comm;
+    int32_t periodic[2];  // i, j: the global domain wraps around (oec_decomp_set_periodic)
 };
 
 namespace oec {
@@ -123,9 +124,12 @@ void subdomain(const int64_t g[3], int px, int py, int rank, int64_t lo[3], int6
 
 namespace {
 
-// messages of `rank` in execution order (see oec.h oec_decomp_plan)
+// messages of `rank` in execution order (see oec.h oec_decomp_plan).  per_i / per_j: periodic
+// global domain in i / j -- the first and last rank of a row (column) of the rank grid are
+// neighbours (the same rank when px (py) == 1); receive boxes then lie outside [0, g) in the
+// receiver's frame and equal the sender's box modulo the period.
 std::vector<oec_halo_msg> make_plan(const int64_t g[3], int px, int py, int rank, const int32_t wlo[3],
-                                    const int32_t whi[3]) {
+                                    const int32_t whi[3], bool per_i = false, bool per_j = false) {
     std::vector<oec_halo_msg> m;
     int64_t lo[3], hi[3];
     subdomain(g, px, py, rank, lo, hi);
@@ -145,23 +149,27 @@ std::vector<oec_halo_msg> make_plan(const int64_t g[3], int px, int py, int rank
         if (a1 > a0 && b1 > b0) m.push_back(x);
     };
     // phase 0: i-neighbours, interior j-range. tags: 0 = towards -i, 1 = towards +i, 2 = -j, 3 = +j
-    if (ri > 0) {  // left neighbour: it needs our first whi[0] columns, we need its last wlo[0]
-        add(rank - 1, 1, 0, 0, lo[0], lo[0] + whi[0], lo[1], hi[1]);
-        add(rank - 1, 0, 0, 1, lo[0] - wlo[0], lo[0], lo[1], hi[1]);
+    const int left = ri > 0 ? rank - 1 : per_i ? rank + px - 1 : -1;
+    const int right = ri < px - 1 ? rank + 1 : per_i ? rank - px + 1 : -1;
+    const int down = rj > 0 ? rank - px : per_j ? rank + (py - 1) * px : -1;
+    const int up = rj < py - 1 ? rank + px : per_j ? rank - (py - 1) * px : -1;
+    if (left >= 0) {  // left neighbour: it needs our first whi[0] columns, we need its last wlo[0]
+        add(left, 1, 0, 0, lo[0], lo[0] + whi[0], lo[1], hi[1]);
+        add(left, 0, 0, 1, lo[0] - wlo[0], lo[0], lo[1], hi[1]);
     }
-    if (ri < px - 1) {
-        add(rank + 1, 1, 0, 1, hi[0] - wlo[0], hi[0], lo[1], hi[1]);
-        add(rank + 1, 0, 0, 0, hi[0], hi[0] + whi[0], lo[1], hi[1]);
+    if (right >= 0) {
+        add(right, 1, 0, 1, hi[0] - wlo[0], hi[0], lo[1], hi[1]);
+        add(right, 0, 0, 0, hi[0], hi[0] + whi[0], lo[1], hi[1]);
     }
     // phase 1: j-neighbours, i-range including the i-halo (corners)
     const int64_t i0 = lo[0] - wlo[0], i1 = hi[0] + whi[0];
-    if (rj > 0) {
-        add(rank - px, 1, 1, 2, i0, i1, lo[1], lo[1] + whi[1]);
-        add(rank - px, 0, 1, 3, i0, i1, lo[1] - wlo[1], lo[1]);
+    if (down >= 0) {
+        add(down, 1, 1, 2, i0, i1, lo[1], lo[1] + whi[1]);
+        add(down, 0, 1, 3, i0, i1, lo[1] - wlo[1], lo[1]);
     }
-    if (rj < py - 1) {
-        add(rank + px, 1, 1, 3, i0, i1, hi[1] - wlo[1], hi[1]);
-        add(rank + px, 0, 1, 2, i0, i1, hi[1], hi[1] + whi[1]);
+    if (up >= 0) {
+        add(up, 1, 1, 3, i0, i1, hi[1] - wlo[1], hi[1]);
+        add(up, 0, 1, 2, i0, i1, hi[1], hi[1] + whi[1]);
     }
     return m;
 }
@@ -239,6 +247,20 @@ oec_status check_widths(const int32_t *wlo, const int32_t *whi) {
     return OEC_OK;
 }
 
+// every box a rank sends must lie in its own sub-domain along the exchanged dimension (i in
+// phase 0, j in phase 1): a halo wider than the neighbour's sub-domain would need two hops
+oec_status check_plan(const int64_t g[3], int px, int py, int rank, const std::vector<oec_halo_msg> &plan) {
+    int64_t lo[3], hi[3];
+    subdomain(g, px, py, rank, lo, hi);
+    for (const auto &m : plan) {
+        const int dim = m.phase;
+        if (m.is_send && (m.lo[dim] < lo[dim] || m.hi[dim] > hi[dim]))
+            return set_error(OEC_ERR_SHAPE, "halo: width exceeds rank %d's sub-domain [%lld,%lld) in dim %d", rank,
+                             (long long)lo[dim], (long long)hi[dim], dim);
+    }
+    return OEC_OK;
+}
+
 // One (message, field) buffer of a rank.  DIRECT: with a j-slab decomposition (px == 1) and a
 // field whose j rows are the slowest dimension (the default i,k,j order, or a k-invariant
 // field), the message's box -- whole j rows, all k, the i range including the i-halo -- lies in
@@ -261,8 +283,8 @@ struct MsgBuf {
 };
 
 template <class T>
-bool span_of(const oec_field *f, const FVT<T> &v, const Box &b, int px, T **p, size_t *count) {
-    if (px != 1) return false;
+bool span_of(const oec_field *f, const FVT<T> &v, const Box &b, int px, int phase, T **p, size_t *count) {
+    if (px != 1 || phase != 1) return false;  // phase 0 (periodic i) boxes are not whole rows
     const bool kinv = is_kinv(f);
     const int64_t ni = f->ub[0] - f->lb[0], nk = f->ub[2] - f->lb[2];
     const int64_t sj = f->stride[1], sk = kinv ? 0 : f->stride[2];
@@ -289,7 +311,7 @@ oec_status rank_buffers(const std::vector<oec_halo_msg> &plan, oec_field *const 
             FVT<T> v;
             oec_status st = view_of(fields[f], &v);
             if (st || (st = field_box(fields[f], plan[q], org, &mb.box))) return st;
-            mb.direct = span_of(fields[f], v, mb.box, px, &mb.ptr, &mb.count);
+            mb.direct = span_of(fields[f], v, mb.box, px, plan[q].phase, &mb.ptr, &mb.count);
             if (!mb.direct) {
                 mb.count = (size_t)box_volume(mb.box);
                 mb.off = *staged;
@@ -322,7 +344,8 @@ oec_status halo_exchange_impl(oec_decomp *d, oec_field *const *fields, int32_t n
                               const int32_t width_hi[3], void *stream) {
     oec_status st = check_widths(width_lo, width_hi);
     if (st) return st;
-    auto plan = make_plan(d->gdom, d->px, d->py, d->rank, width_lo, width_hi);
+    auto plan = make_plan(d->gdom, d->px, d->py, d->rank, width_lo, width_hi, d->periodic[0], d->periodic[1]);
+    if ((st = check_plan(d->gdom, d->px, d->py, d->rank, plan))) return st;
     set_launch_count(0);
     if (plan.empty() || n == 0) return OEC_OK;
     if (!d->comm) return set_error(OEC_ERR_NCCL, "oec_halo_exchange: decomposition has no NCCL communicator");
@@ -343,6 +366,17 @@ oec_status halo_exchange_impl(oec_decomp *d, oec_field *const *fields, int32_t n
             if (!mb.direct) mb.ptr = stage + mb.off;
     }
     constexpr int NCCL_DT = sizeof(T) == 8 ? NCCL_FLOAT64 : NCCL_FLOAT32;
+    // NCCL matches the sends and receives between two ranks in issue order (no tags): issue each
+    // peer's messages by (tag, field) on both sides -- with a periodic domain a peer can be both
+    // neighbours (px == 2) or this rank itself (px == 1), so plan order alone would not match
+    std::vector<size_t> order(bufs.size());
+    for (size_t q = 0; q < order.size(); ++q) order[q] = q;
+    std::stable_sort(order.begin(), order.end(), [&](size_t a, size_t b) {
+        const MsgBuf<T> &x = bufs[a], &y = bufs[b];
+        if (x.m.peer != y.m.peer) return x.m.peer < y.m.peer;
+        if (x.m.tag != y.m.tag) return x.m.tag < y.m.tag;
+        return x.field < y.field;
+    });
     int launches = 0;
     oec_status result = OEC_OK;
     for (int phase = 0; phase < 2 && result == OEC_OK; ++phase) {
@@ -352,7 +386,8 @@ oec_status halo_exchange_impl(oec_decomp *d, oec_field *const *fields, int32_t n
             break;
         }
         int r = g_nccl.gstart();
-        for (auto &mb : bufs) {
+        for (size_t q : order) {
+            const MsgBuf<T> &mb = bufs[q];
             if (r != 0) break;
             if (mb.m.phase != phase) continue;
             r = mb.m.is_send ? g_nccl.send(mb.ptr, mb.count, NCCL_DT, mb.m.peer, d->comm, s)
@@ -376,8 +411,9 @@ oec_status halo_exchange_impl(oec_decomp *d, oec_field *const *fields, int32_t n
 // a device-to-device copy from the sender's buffer (its staging or its field span) into the
 // receiver's, in place of ncclSend / ncclRecv.  Tests the whole exchange but the NCCL calls.
 template <class T>
-oec_status halo_exchange_local_impl(const int64_t global_domain[3], int32_t px, int32_t py, oec_field *const *fields,
-                                    int32_t n, const int32_t width_lo[3], const int32_t width_hi[3], void *stream) {
+oec_status halo_exchange_local_impl(const int64_t global_domain[3], int32_t px, int32_t py, const int32_t *periodic,
+                                    oec_field *const *fields, int32_t n, const int32_t width_lo[3],
+                                    const int32_t width_hi[3], void *stream) {
     oec_status st = check_widths(width_lo, width_hi);
     if (st) return st;
     cudaStream_t s = (cudaStream_t)stream;
@@ -388,7 +424,8 @@ oec_status halo_exchange_local_impl(const int64_t global_domain[3], int32_t px, 
     for (int r = 0; r < R; ++r) {
         int64_t org[3], tmp[3];
         subdomain(global_domain, px, py, r, org, tmp);
-        auto plan = make_plan(global_domain, px, py, r, width_lo, width_hi);
+        auto plan = make_plan(global_domain, px, py, r, width_lo, width_hi, periodic && periodic[0], periodic && periodic[1]);
+        if ((st = check_plan(global_domain, px, py, r, plan))) return st;
         if ((st = rank_buffers(plan, fields + (size_t)r * n, n, org, px, &bufs[r], &staged[r]))) return st;
         total += staged[r];
     }
@@ -451,10 +488,18 @@ oec_status oec_decomp_create(const int64_t global_domain[3], int32_t px, int32_t
     d->ri = rank % px;
     d->rj = rank / px;
     d->comm = nccl_comm;
+    d->periodic[0] = d->periodic[1] = 0;
     subdomain(global_domain, px, py, rank, d->lo, d->hi);
     if (local_lb) memcpy(local_lb, d->lo, sizeof d->lo);
     if (local_ub) memcpy(local_ub, d->hi, sizeof d->hi);
     *out = d;
+    return OEC_OK;
+}
+
+oec_status oec_decomp_set_periodic(oec_decomp *d, int32_t periodic_i, int32_t periodic_j) {
+    if (!d) return set_error(OEC_ERR_ARG, "oec_decomp_set_periodic: NULL decomposition");
+    d->periodic[0] = periodic_i != 0;
+    d->periodic[1] = periodic_j != 0;
     return OEC_OK;
 }
 
@@ -468,7 +513,7 @@ oec_status oec_decomp_plan(const oec_decomp *d, const int32_t width_lo[3], const
     if (!d || !n_msgs) return set_error(OEC_ERR_ARG, "oec_decomp_plan: NULL argument");
     oec_status st = check_widths(width_lo, width_hi);
     if (st) return st;
-    auto m = make_plan(d->gdom, d->px, d->py, d->rank, width_lo, width_hi);
+    auto m = make_plan(d->gdom, d->px, d->py, d->rank, width_lo, width_hi, d->periodic[0], d->periodic[1]);
     *n_msgs = (int32_t)m.size();
     for (int32_t q = 0; q < (int32_t)m.size() && q < capacity && msgs; ++q) msgs[q] = m[q];
     return OEC_OK;
@@ -482,13 +527,19 @@ oec_status oec_halo_exchange(oec_decomp *d, oec_field *const *fields, int32_t n,
     return halo_exchange_impl<double>(d, fields, n, width_lo, width_hi, stream);
 }
 
-oec_status oec_halo_exchange_local(const int64_t global_domain[3], int32_t px, int32_t py, oec_field *const *fields,
-                                   int32_t n, const int32_t width_lo[3], const int32_t width_hi[3], void *stream) {
+oec_status oec_halo_exchange_local_periodic(const int64_t global_domain[3], int32_t px, int32_t py,
+                                            const int32_t periodic[2], oec_field *const *fields, int32_t n,
+                                            const int32_t width_lo[3], const int32_t width_hi[3], void *stream) {
     if (!global_domain || !fields || n < 1 || px < 1 || py < 1 || !fields[0])
         return set_error(OEC_ERR_ARG, "oec_halo_exchange_local: bad arguments");
     if (fields[0]->dtype == OEC_F32)
-        return halo_exchange_local_impl<float>(global_domain, px, py, fields, n, width_lo, width_hi, stream);
-    return halo_exchange_local_impl<double>(global_domain, px, py, fields, n, width_lo, width_hi, stream);
+        return halo_exchange_local_impl<float>(global_domain, px, py, periodic, fields, n, width_lo, width_hi, stream);
+    return halo_exchange_local_impl<double>(global_domain, px, py, periodic, fields, n, width_lo, width_hi, stream);
+}
+
+oec_status oec_halo_exchange_local(const int64_t global_domain[3], int32_t px, int32_t py, oec_field *const *fields,
+                                   int32_t n, const int32_t width_lo[3], const int32_t width_hi[3], void *stream) {
+    return oec_halo_exchange_local_periodic(global_domain, px, py, nullptr, fields, n, width_lo, width_hi, stream);
 }
 
 }  // extern "C"

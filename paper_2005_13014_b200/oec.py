@@ -99,6 +99,10 @@ SIGNATURES = {
     "oec_halo_exchange": (C.c_int, [C.c_void_p, _PP, C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.c_void_p]),
     "oec_halo_exchange_local": (C.c_int, [C.POINTER(C.c_int64), C.c_int32, C.c_int32, _PP, C.c_int32,
                                           C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.c_void_p]),
+    "oec_halo_exchange_local_periodic": (C.c_int, [C.POINTER(C.c_int64), C.c_int32, C.c_int32, C.POINTER(C.c_int32),
+                                                   _PP, C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_int32),
+                                                   C.c_void_p]),
+    "oec_decomp_set_periodic": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32]),
     "oec_decomp_destroy": (C.c_int, [C.c_void_p]),
     "oec_hdiff_pipeline_create": (C.c_int, [C.POINTER(C.c_int64), C.c_int32, C.c_int32, C.c_int32, _P, _P, _P,
                                             C.POINTER(C.c_void_p)]),
@@ -451,6 +455,10 @@ def oec_decomp_create(global_domain, px: int, py: int, rank: int, nccl_comm: Opt
     return Decomp(h, lo, hi)
 
 
+def oec_decomp_set_periodic(d: Decomp, periodic_i: bool, periodic_j: bool):
+    _check(lib().oec_decomp_set_periodic(d.handle, int(bool(periodic_i)), int(bool(periodic_j))))
+
+
 def oec_decomp_plan(d: Decomp, width_lo, width_hi) -> List[dict]:
     n = C.c_int32()
     _check(lib().oec_decomp_plan(d.handle, _i32(width_lo), _i32(width_hi), None, 0, C.byref(n)))
@@ -466,10 +474,15 @@ def oec_halo_exchange(d: Decomp, fields: Sequence[Field], width_lo, width_hi, st
 
 
 def oec_halo_exchange_local(global_domain, px: int, py: int, fields: Sequence[Field], n_per_rank: int, width_lo,
-                            width_hi, stream=None):
+                            width_hi, stream=None, periodic=None):
     arr = (_P * len(fields))(*[f.ptr for f in fields])
-    _check(lib().oec_halo_exchange_local(_i64(global_domain), px, py, arr, n_per_rank, _i32(width_lo), _i32(width_hi),
-                                         _stream(stream)))
+    if periodic is None:
+        _check(lib().oec_halo_exchange_local(_i64(global_domain), px, py, arr, n_per_rank, _i32(width_lo),
+                                             _i32(width_hi), _stream(stream)))
+    else:
+        per = (C.c_int32 * 2)(int(bool(periodic[0])), int(bool(periodic[1])))
+        _check(lib().oec_halo_exchange_local_periodic(_i64(global_domain), px, py, per, arr, n_per_rank,
+                                                      _i32(width_lo), _i32(width_hi), _stream(stream)))
 
 
 def oec_selftest_rcp32():

@@ -217,3 +217,46 @@ def test_plan_consistency(g, px, py, w):
                     assert got == 1, (r, i, j)
                 elif (lo[1] <= j < hi[1]) or not (0 <= j < g[1]):
                     assert got == 0 or in_i_halo_of_global
+
+
+@pytest.mark.parametrize("g,px,py,per", [((16, 16, 3), 2, 2, (True, True)), ((17, 13, 2), 3, 2, (True, False)),
+                                         ((12, 9, 2), 1, 1, (True, True)), ((12, 9, 2), 2, 1, (True, True)),
+                                         ((32, 64, 4), 1, 8, (False, True))])
+def test_periodic_plan_consistency(g, px, py, per):
+    # periodic: every recv of r from p (phase, tag) pairs with exactly one send of p to r whose box
+    # equals it modulo the period, and every halo cell of every rank is received exactly once
+    # (in-domain cells and, across a periodic boundary, the wrapped ones)
+    wlo, whi = (2, 1, 0), (1, 2, 0)
+    R = px * py
+    decs = [oec.oec_decomp_create(g, px, py, r) for r in range(R)]
+    for d in decs:
+        oec.oec_decomp_set_periodic(d, *per)
+    plans = [oec.oec_decomp_plan(d, wlo, whi) for d in decs]
+
+    def wrap(lo, hi):
+        return tuple((lo[d] % g[d], hi[d] - lo[d]) if d < 2 and per[d] else (lo[d], hi[d] - lo[d]) for d in range(3))
+
+    for r in range(R):
+        for m in plans[r]:
+            if m["is_send"]:
+                continue
+            match = [x for x in plans[m["peer"]] if x["is_send"] and x["peer"] == r and x["phase"] == m["phase"]
+                     and x["tag"] == m["tag"]]
+            assert len(match) == 1, (r, m)
+            assert wrap(match[0]["lo"], match[0]["hi"]) == wrap(m["lo"], m["hi"]), (r, m, match[0])
+    for r, d in enumerate(decs):
+        lo, hi = d.local_lb, d.local_ub
+        got = {}
+        for m in plans[r]:
+            if not m["is_send"]:
+                for j in range(m["lo"][1], m["hi"][1]):
+                    for i in range(m["lo"][0], m["hi"][0]):
+                        got[(i, j)] = got.get((i, j), 0) + 1
+        for j in range(lo[1] - wlo[1], hi[1] + whi[1]):
+            for i in range(lo[0] - wlo[0], hi[0] + whi[0]):
+                own = lo[0] <= i < hi[0] and lo[1] <= j < hi[1]
+                reach = (per[0] or 0 <= i < g[0]) and (per[1] or 0 <= j < g[1])
+                if own:
+                    assert got.get((i, j), 0) == 0
+                elif reach:
+                    assert got.get((i, j), 0) == 1, (r, i, j)

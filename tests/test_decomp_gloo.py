@@ -44,7 +44,20 @@ def _local_field(g: HostField, org, lo_local, hi_local, fill=np.nan):
     return loc
 
 
-def _worker(rank, world, port, program, gdom, px, py, wlo, whi, q):
+def _wrapped(host, gdom, per):
+    """Global inputs with the halo cells of periodic dimensions replaced by the interior cells they
+    wrap to (the definition of a periodic domain)."""
+    out = {}
+    for name, g in host.items():
+        sj = np.arange(g.lb[1], g.ub[1])
+        si = np.arange(g.lb[0], g.ub[0])
+        sj = (np.mod(sj, gdom[1]) if per[1] else sj) - g.lb[1]
+        si = (np.mod(si, gdom[0]) if per[0] else si) - g.lb[0]
+        out[name] = HostField(np.ascontiguousarray(g.data[:, sj][:, :, si]), g.lb, g.ub, g.k_invariant)
+    return out
+
+
+def _worker(rank, world, port, program, gdom, px, py, wlo, whi, q, per=(False, False)):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -52,6 +65,7 @@ def _worker(rank, world, port, program, gdom, px, py, wlo, whi, q):
         from paper_2005_13014_b200 import oec
 
         dec = oec.oec_decomp_create(gdom, px, py, rank)
+        oec.oec_decomp_set_periodic(dec, *per)
         lo, hi = dec.local_lb, dec.local_ub
         ldom = tuple(hi[d] - lo[d] for d in range(3))
         host = synth.make_inputs(program, gdom, seed=3)
@@ -68,7 +82,7 @@ def _worker(rank, world, port, program, gdom, px, py, wlo, whi, q):
                     for ii in range(llo[0], lhi[0]):
                         gi, gj = ii + lo[0], jj + lo[1]
                         own = 0 <= ii < ldom[0] and 0 <= jj < ldom[1]
-                        outside = not (0 <= gi < gdom[0] and 0 <= gj < gdom[1])
+                        outside = (not per[0] and not 0 <= gi < gdom[0]) or (not per[1] and not 0 <= gj < gdom[1])
                         if own or outside:
                             f.data[k - llo[2], jj - llo[1], ii - llo[0]] = g.data[k - g.lb[2], gj - g.lb[1], gi - g.lb[0]]
             local[s.name] = f
@@ -77,26 +91,32 @@ def _worker(rank, world, port, program, gdom, px, py, wlo, whi, q):
         # exchange the fields whose halo covers the exchange widths (hdiff: `in`; vadv with an i-split: wcon)
         halo_fields = [s.name for s in spec.inputs if not s.k_invariant
                        and all(s.halo_lo[d] >= wlo[d] and s.halo_hi[d] >= whi[d] for d in (0, 1))]
+        # (tagged by plan tag and field: with a periodic domain one peer can be both neighbours;
+        # messages to this rank itself are copied locally)
         for phase in (0, 1):
-            reqs, recvs = [], []
+            reqs, recvs, own = [], [], {}
             for m in plan:
                 if m["phase"] != phase:
                     continue
-                for name in halo_fields:
+                for fi, name in enumerate(halo_fields):
                     f = local[name]
                     blo = (m["lo"][0] - lo[0], m["lo"][1] - lo[1], f.lb[2])
                     bhi = (m["hi"][0] - lo[0], m["hi"][1] - lo[1], f.ub[2])
                     sl = _box_slices(f, blo, bhi)
-                    if m["is_send"]:
-                        reqs.append(dist.isend(torch.from_numpy(np.ascontiguousarray(f.data[sl])), m["peer"]))
+                    tag = 16 * m["tag"] + fi
+                    if m["is_send"] and m["peer"] == rank:
+                        own[tag] = np.ascontiguousarray(f.data[sl])
+                    elif m["is_send"]:
+                        reqs.append(dist.isend(torch.from_numpy(np.ascontiguousarray(f.data[sl])), m["peer"], tag=tag))
                     else:
                         buf = torch.empty(f.data[sl].shape, dtype=torch.float64)
-                        reqs.append(dist.irecv(buf, m["peer"]))
-                        recvs.append((f, sl, buf))
+                        if m["peer"] != rank:
+                            reqs.append(dist.irecv(buf, m["peer"], tag=tag))
+                        recvs.append((f, sl, buf, tag, m["peer"] == rank))
             for r in reqs:
                 r.wait()
-            for f, sl, buf in recvs:
-                f.data[sl] = buf.numpy()
+            for f, sl, buf, tag, self_msg in recvs:
+                f.data[sl] = own[tag] if self_msg else buf.numpy()
         # no NaN may remain in what the program reads
         sc = synth.scalars(program)
         out = HostField(np.full((ldom[2], ldom[1], ldom[0]), np.nan), (0, 0, 0), ldom)
@@ -105,6 +125,7 @@ def _worker(rank, world, port, program, gdom, px, py, wlo, whi, q):
         else:
             capi.vadv(local, out, sc["dtr_stage"], (0, 0, 0), ldom)
         gout = HostField(np.full((gdom[2], gdom[1], gdom[0]), np.nan), (0, 0, 0), gdom)
+        host = _wrapped(host, gdom, per)
         if program == "hdiff":
             capi.hdiff(host["in"], host["coeff"], gout, (0, 0, 0), gdom)
         else:
@@ -124,11 +145,26 @@ def _worker(rank, world, port, program, gdom, px, py, wlo, whi, q):
     ("vadv", (14, 5, 6), 2, 1, ((0, 0, 0), (1, 0, 0))),
 ])
 def test_decomposed_equals_global(program, gdom, px, py, w):
+    _run(program, gdom, px, py, w, (False, False))
+
+
+@pytest.mark.parametrize("program,gdom,px,py,w,per", [
+    ("hdiff", (12, 10, 2), 2, 1, ((2, 2, 0), (2, 2, 0)), (True, True)),  # the same peer on both sides in i
+    ("hdiff", (13, 11, 2), 2, 2, ((2, 2, 0), (2, 2, 0)), (True, True)),
+    ("vadv", (14, 5, 6), 2, 1, ((0, 0, 0), (1, 0, 0)), (True, False)),
+])
+def test_periodic_decomposed_equals_wrapped_global(program, gdom, px, py, w, per):
+    # periodic domain (oec_decomp_set_periodic): the result equals the oracle on the global field
+    # whose halo is the wrapped interior
+    _run(program, gdom, px, py, w, per)
+
+
+def _run(program, gdom, px, py, w, per):
     world = px * py
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, program, gdom, px, py, w[0], w[1], q))
+    procs = [ctx.Process(target=_worker, args=(r, world, port, program, gdom, px, py, w[0], w[1], q, per))
              for r in range(world)]
     for p in procs:
         p.start()

@@ -7,7 +7,8 @@ capture runs three kernels in a row with --cache-control none:
     evict (a read of 4x L2: L2 left clean)  ->  the program's kernel  ->  evict again
 
 and traffic = kernel dram read + kernel dram write + the second evict's dram write (the kernel's
-write-back: the evict kernels themselves write nothing).
+write-back) minus an evict's own writes after a clean L2 (measured first: three evicts in a row;
+round-2 captures showed ~1.7-2 MB per evict that is not the kernel's output).
 
     # on the GPU box
     ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum \
@@ -38,6 +39,12 @@ def run(cfg):
     dom, progs = CONFIGS[cfg]
     l2 = torch.cuda.get_device_properties(0).L2_cache_size
     evict = torch.zeros(4 * l2 // 8, dtype=torch.float64, device="cuda")
+    # baseline: three evicts back to back -- the DRAM writes of an evict that follows a clean L2
+    # (its own partial sums and whatever else the driver writes back) are subtracted from the
+    # write-back charged to the evict after each kernel
+    for _ in range(3):
+        evict.sum()
+    torch.cuda.synchronize()
     for p in progs:
         spec = synth.PROGRAMS[p]
         host = synth.make_inputs(p, dom, seed=0)
@@ -70,11 +77,17 @@ def parse(path, cfg):
 
     def to_bytes(v):
         x, u = v
-        return x * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1)
+        return x * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6, "GB": 1e9}.get(u, 1)
 
     dom, progs = CONFIGS[cfg]
     out = {}
     q = 0
+    while q < len(seq) and "reduce" not in seq[q][0].lower():
+        q += 1
+    base = 0.0
+    if all("reduce" in seq[q + t][0].lower() for t in range(3)):  # the baseline evicts (run())
+        base = 0.5 * (to_bytes(seq[q + 1][1]["dram__bytes_write.sum"]) + to_bytes(seq[q + 2][1]["dram__bytes_write.sum"]))
+        q += 3
     for p in progs:
         # skip the warm-up launches until the reduce that precedes the timed kernel
         while q < len(seq) and "reduce" not in seq[q][0].lower():
@@ -84,7 +97,7 @@ def parse(path, cfg):
         rd_b, wr_b = to_bytes(m["dram__bytes_read.sum"]), to_bytes(m["dram__bytes_write.sum"])
         wb = to_bytes(after["dram__bytes_write.sum"])
         out[p] = {"kernel": name[:80], "read": rd_b, "write_in_kernel": wr_b, "write_back_after": wb,
-                  "traffic": rd_b + wr_b + wb, "duration_us": m["gpu__time_duration.sum"][0] / (1e3 if m["gpu__time_duration.sum"][1] == "nsecond" else 1)}
+                  "evict_baseline_write": base, "traffic": rd_b + wr_b + max(0.0, wb - base), "duration_us": m["gpu__time_duration.sum"][0] / (1e3 if m["gpu__time_duration.sum"][1] in ("ns", "nsecond") else 1)}
         q += 3
     dst = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     allv = {}
