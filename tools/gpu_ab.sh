@@ -10,7 +10,7 @@ OUT=gpurun_out/ab_${TAG:-x}.jsonl
 for rep in 1 2 3; do
   for v in ${VARIANTS:-old new}; do
     for dom in $DOMS; do
-      OEC_LIB_PATH=tune/liboec_$v.so timeout 300 python tools/kernel_bench.py --programs $PROGS --domain ${dom//,/ } --tag $v >> $OUT 2>&1
+      OEC_LIB_PATH=tune/liboec_$v.so timeout 300 python tools/kernel_bench.py --programs $PROGS --domain ${dom//,/ } --dtype ${DTYPE:-f64} --tag $v >> $OUT 2>&1
     done
   done
 done

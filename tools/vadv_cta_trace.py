@@ -18,17 +18,19 @@ import synth  # noqa: E402
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--domain", type=int, nargs=3, default=[128, 128, 80])
+    ap.add_argument("--dtype", default="f64", choices=["f64", "f32"])
     a = ap.parse_args()
     import torch
 
     from paper_2005_13014_b200 import oec
 
     dom = tuple(a.domain)
-    host = synth.make_inputs("vadv", dom, seed=0)
+    dt = np.float32 if a.dtype == "f32" else np.float64
+    host = synth.make_inputs("vadv", dom, seed=0, dtype=dt)
     sets = []
     for _ in range(8):
         ins = [oec.field_from_host(host[s.name]) for s in synth.PROGRAMS["vadv"].inputs]
-        sets.append((ins, [oec.empty_like_domain(dom, fill=0.0)]))
+        sets.append((ins, [oec.empty_like_domain(dom, fill=0.0, dtype=dt)]))
     for rep in range(3):
         for r in range(8):
             oec.oec_apply_program("vadv", sets[r][0], sets[r][1], [0.15], (0, 0, 0), dom)
@@ -40,7 +42,7 @@ def main():
     t = t[:, :ncta]
     t0 = t[0].min()
     names = ["start", "first chunk", "forward done", "end"]
-    print(f"domain {dom}, {ncta} CTAs; times in us after the earliest CTA start")
+    print(f"domain {dom} {a.dtype}, {ncta} CTAs; times in us after the earliest CTA start")
     for e in range(4):
         q = np.quantile((t[e] - t0) / 1e3, [0, 0.1, 0.5, 0.9, 1.0])
         print(f"{names[e]:14s} min {q[0]:6.2f}  p10 {q[1]:6.2f}  med {q[2]:6.2f}  p90 {q[3]:6.2f}  max {q[4]:6.2f}")
