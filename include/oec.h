@@ -367,8 +367,9 @@ oec_status oec_decomp_destroy(oec_decomp *d);
  * stays inside the sub-domain stream through the TMA ring first; the boundary tiles then read
  * the neighbours' cells of x_t directly from the neighbours' x0/x1 (device pointers valid on this
  * device: NVLink peer memory imported with oec_ipc_import, or plain pointers when the sub-domains
- * share a device), after the neighbours have signalled (st.release.sys into this rank's signal
- * pad) that step t-1 is complete.  No halo is copied and there is no exchange launch; the
+ * share a device), after the neighbours have signalled (each of their CTAs adds its share of
+ * 2^20 with red.release.sys into this rank's signal pad; no returning atomic) that step t-1 is
+ * complete.  No halo is copied and there is no exchange launch; the
  * transfer overlaps the interior tiles.  The step counter t lives in device memory, so a CUDA
  * graph of captured oec_hdiff_pipeline_run calls advances on every replay.
  *

@@ -629,28 +629,32 @@ cudaError_t launch_tma(const TMap &tin, const TMap &tcf, const FOT<T> &out, cons
 // shared memory with plain loads -- our cells from our field, the neighbours' cells straight from
 // THEIR fields (peer memory over NVLink, or the same device) -- and runs the same tile code.  No
 // halo is copied, no exchange kernel or NCCL call exists, and the transfer overlaps the interior.
-// When all CTAs are done the last one publishes t+1 into each neighbour's signal pad
-// (st.release.sys) and advances our step counter.  Safety: a neighbour's step t+1 overwrites the
-// buffer we read at step t only in its boundary tiles, which wait for our "step t done".
+// Step counting without a returning atomic: every CTA, once its warps are done, adds its share
+// w_b of 2^20 (the shares of a grid sum to exactly 2^20, whatever its size) to our FINISHED word
+// (relaxed: read by our next step after griddepcontrol.wait, i.e. after this grid completed, so
+// t = FINISHED >> 20) and to each neighbour's word for us (red.release.sys: the neighbour's
+// boundary tiles of step t+1 wait until it reaches (t+1) << 20).  Safety: a neighbour's step t+1
+// overwrites the buffer we read at step t only in its boundary tiles, which wait for our "step t
+// done".  (Round 1 counted CTAs with acq_rel atomics and let the last one publish: the returning
+// atomics of 148 CTAs on one word cost 0.85 us per step at 128^2.)
 __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long *p) {
     unsigned long long v;
     asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
 }
-__device__ __forceinline__ void st_release_sys(unsigned long long *p, unsigned long long v) {
-    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+__device__ __forceinline__ void red_release_sys(unsigned long long *p, unsigned long long v) {
+    asm volatile("red.release.sys.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
+__device__ __forceinline__ void red_relaxed_gpu(unsigned long long *p, unsigned long long v) {
+    asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+constexpr int PIPE_STEP_SHIFT = 20;  // one completed step = 2^20 in a FINISHED / neighbour word
 
 // "step done" counting: acq_rel atomics (PTX release is cumulative over everything that
 // happens-before it, acquire makes the other arrivals' prior accesses visible to the last one)
 __device__ __forceinline__ unsigned atom_add_acqrel_cta_shared(unsigned *p, unsigned v) {
     unsigned old;
     asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(smem_u32(p)), "r"(v) : "memory");
-    return old;
-}
-__device__ __forceinline__ unsigned long long atom_add_acqrel_sys(unsigned long long *p, unsigned long long v) {
-    unsigned long long old;
-    asm volatile("atom.acq_rel.sys.global.add.u64 %0, [%1], %2;" : "=l"(old) : "l"(p), "l"(v) : "memory");
     return old;
 }
 __device__ __forceinline__ unsigned long long atom_add_relaxed_gpu(unsigned long long *p, unsigned long long v) {
@@ -707,16 +711,19 @@ __global__ void __launch_bounds__(NW * 32, 1) hdiff_pipe(const __grid_constant__
         prefetch_tmap(&m_cf.map);
     }
     if (threadIdx.x == 0) *warps_done = 0;
+    unsigned long long tg = 0;  // the guessed step t (lane 0)
     if (lane == 0) {
         // warm L2 with the first interior tiles during the previous kernel's drain: coefficients,
         // and x_t of the GUESSED step t.  The guess reads the pad before griddepcontrol.wait, so
-        // it may be stale; it only selects what to prefetch -- the loads below use t read after
-        // the wait.  If this pipeline's previous step is still draining (this CTA only got an SM
-        // because one of its CTAs exited, having counted itself in FINISHED), t is one ahead of
-        // the pad's STEP word.
-        const unsigned long long fin = *reinterpret_cast<volatile const unsigned long long *>(a.pad + PIPE_PAD_FINISHED);
-        const unsigned long long tg =
-            *reinterpret_cast<volatile const unsigned long long *>(a.pad + PIPE_PAD_STEP) + (fin != 0 ? 1 : 0);
+        // it may be stale; it selects what to prefetch and which buffer the first tiles are
+        // requested from -- the step t read after the wait decides.  If this pipeline's previous
+        // step is still draining (this CTA only got an SM because one of its CTAs exited, having
+        // added its share), FINISHED is between two multiples of 2^20: rounding up gives t.
+        static_assert(PIPE_PAD_FINISHED % 2 == 0 && PIPE_PAD_FLIP == PIPE_PAD_FINISHED + 1, "pad layout");
+        unsigned long long fin, flip;
+        asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(fin), "=l"(flip) : "l"(a.pad + PIPE_PAD_FINISHED));
+        tg = (fin + (1ull << PIPE_STEP_SHIFT) - 1) >> PIPE_STEP_SHIFT;
+        tg ^= flip & 1;
         const TMap &mg = (tg & 1) ? m1 : m0;
         const int ns = a.sb - a.sa, nc = a.cb - a.ca;
         for (int q = 0; q < S; ++q) {
@@ -728,14 +735,15 @@ __global__ void __launch_bounds__(NW * 32, 1) hdiff_pipe(const __grid_constant__
             }
         }
     }
+    if (lane == 0) {
+#pragma unroll
+        for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
+        fence_mbar_init();
+    }
     __syncthreads();
     griddep_launch_dependents();
     griddep_wait();
-    const unsigned long long t = *reinterpret_cast<volatile const unsigned long long *>(a.pad + PIPE_PAD_STEP);
-    const int b = (int)(t & 1);
-    const TMap &m_in = b ? m1 : m0;
-    const FOT<T> out = a.y[b ^ 1];
-    const int nk = a.d.hi[2];
+    const int gb = (int)(__shfl_sync(0xffffffffu, tg, 0) & 1);  // guessed parity
 
     auto in_s = [&](int s) { return reinterpret_cast<T *>(wbase + s * C::SLOT); };
     auto cf_s = [&](int s) { return reinterpret_cast<T *>(wbase + s * C::SLOT + C::IN_PAD); };
@@ -745,25 +753,42 @@ __global__ void __launch_bounds__(NW * 32, 1) hdiff_pipe(const __grid_constant__
         j0 = (a.ca + (item / ns_int) % nc_int) * JB;
         k = item / (ns_int * nc_int);
     };
-    auto issue = [&](int item, int s) {
+    auto issue_from = [&](const TMap &mx, int item, int s) {
         int ib, j0, k;
         decode_int(item, ib, j0, k);
         mbar_expect_tx(&bars[s], C::IN_BYTES + C::CF_BYTES);
-        tma_load_ijk(in_s(s), m_in, &bars[s], ib - C::LP, j0 - 2, k);
+        tma_load_ijk(in_s(s), mx, &bars[s], ib - C::LP, j0 - 2, k);
         tma_load_ijk(cf_s(s), m_cf, &bars[s], ib, j0, k);
     };
-
-    if (lane == 0) {
-#pragma unroll
-        for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
-        fence_mbar_init();
-    }
-    // ---- interior tiles: the TMA ring of hdiff_tma
+    // ---- interior tiles: the TMA ring of hdiff_tma.  The first S tiles are requested from the
+    // GUESSED x_t right after griddepcontrol.wait, while the step counter is read (an L2 round
+    // trip otherwise on the critical path); a wrong guess (never in steady state) drains those
+    // loads and requests the tiles again from the right buffer, the ring's phases shifted by one.
     const int n_int = a.n_int;
     if (lane == 0) {
 #pragma unroll
         for (int s = 0; s < S; ++s)
-            if (gw + s * nwt < n_int) issue(gw + s * nwt, s);
+            if (gw + s * nwt < n_int) issue_from(gb ? m1 : m0, gw + s * nwt, s);
+    }
+    const unsigned long long t =
+        *reinterpret_cast<volatile const unsigned long long *>(a.pad + PIPE_PAD_FINISHED) >> PIPE_STEP_SHIFT;
+    const int b = (int)(t & 1);
+    const TMap &m_in = b ? m1 : m0;
+    const FOT<T> out = a.y[b ^ 1];
+    const int nk = a.d.hi[2];
+    auto issue = [&](int item, int s) { issue_from(m_in, item, s); };
+    int poff = 0;
+    if (b != gb) {
+        if (lane == 0) {
+            atom_add_relaxed_gpu(a.pad + PIPE_PAD_MISGUESS, 1ull);
+#pragma unroll
+            for (int s = 0; s < S; ++s)
+                if (gw + s * nwt < n_int) {
+                    mbar_wait(&bars[s], 0);
+                    issue(gw + s * nwt, s);
+                }
+        }
+        poff = 1;
     }
     __syncwarp();
     int n = 0;
@@ -774,7 +799,7 @@ __global__ void __launch_bounds__(NW * 32, 1) hdiff_pipe(const __grid_constant__
         const int nrows = min(JB, a.d.hi[1] - j0);
         const int i_own = ib + lane * V;
         T *out_k = out.p + k * out.sk;
-        mbar_wait(&bars[s], (n / S) & 1);
+        mbar_wait(&bars[s], ((n / S) + poff) & 1);
         if (nrows == JB)
             hdiff_tile<T, V, JB, C::LP, true>(in_s(s), cf_s(s), out_k, out.sj, j0, JB, i_own, a.d.hi[0], lane);
         else
@@ -802,7 +827,7 @@ __global__ void __launch_bounds__(NW * 32, 1) hdiff_pipe(const __grid_constant__
                 const unsigned long long t0 = globaltimer_ns();
                 for (int dd = 0; dd < 9; ++dd)
                     if (a.nb[dd].exists)
-                        while (ld_acquire_sys(a.pad + dd) < t) {
+                        while (ld_acquire_sys(a.pad + dd) < (t << PIPE_STEP_SHIFT)) {
                             __nanosleep(64);
                             if (globaltimer_ns() - t0 > PIPE_WAIT_NS) __trap();
                         }
@@ -848,23 +873,18 @@ __global__ void __launch_bounds__(NW * 32, 1) hdiff_pipe(const __grid_constant__
     }
     (void)nk;
     // ---- publish "step t done" (our outputs written, our reads of the neighbours' x_t finished)
-    // without a CTA barrier: each warp arrives on a per-CTA shared counter (acq_rel, CTA scope);
-    // the CTA's last warp arrives on the global counter -- acq_rel at system scope when there are
-    // neighbours (they read our x_{t+1} and overwrite the x_t we read), relaxed without: then only
-    // the next step of this grid reads our outputs, after griddepcontrol.wait, i.e. after this
-    // grid completed -- and the grid's last arrival publishes t+1 to the neighbours (release,
-    // system scope) and advances the step counter
+    // without a CTA barrier: each warp arrives on a per-CTA shared counter (acq_rel, CTA scope, so
+    // the last warp's release below is cumulative over every warp's accesses); the CTA's last warp
+    // adds the CTA's share -- fire and forget, no round trip
     __syncwarp();
     if (lane == 0 && atom_add_acqrel_cta_shared(warps_done, 1u) == NW - 1) {
-        const unsigned long long old = any_nb ? atom_add_acqrel_sys(a.pad + PIPE_PAD_FINISHED, 1ull)
-                                              : atom_add_relaxed_gpu(a.pad + PIPE_PAD_FINISHED, 1ull);
-        if (old == gridDim.x - 1) {
-            a.pad[PIPE_PAD_FINISHED] = 0;
-            for (int dd = 0; dd < 9; ++dd)
-                if (a.nb[dd].exists) st_release_sys(a.nb[dd].flag, t + 1);
-            *reinterpret_cast<volatile unsigned long long *>(a.pad + PIPE_PAD_STEP) = t + 1;
-        }
+        const unsigned G = gridDim.x, unit = 1u << PIPE_STEP_SHIFT;
+        const unsigned long long w = unit / G + (blockIdx.x < unit % G ? 1u : 0u);
+        for (int dd = 0; dd < 9; ++dd)
+            if (a.nb[dd].exists) red_release_sys(a.nb[dd].flag, w);
+        red_relaxed_gpu(a.pad + PIPE_PAD_FINISHED, w);
     }
+    (void)any_nb;
 }
 
 template <class T, int V, int JB, int S, int NW>

@@ -97,7 +97,12 @@ struct PeerNb {
     int32_t exists, pad_;
 };
 // signal pad words (device memory of the rank that owns the pipeline)
-enum { PIPE_PAD_STEP = 9, PIPE_PAD_FINISHED = 10, PIPE_PAD_WORDS = 16 };
+// PIPE_PAD_MISGUESS: warps that requested their first tiles from the wrong x_t (diagnostics);
+// PIPE_PAD_FLIP != 0: the kernel inverts its guess (tests of the recovery path; 0 from creation)
+// Words 0-8: steps completed by the neighbour in direction d, 2^20 per step; FINISHED: our own
+// steps, 2^20 per step (each CTA adds its share; hdiff.cu).  (FINISHED and FLIP share one 16-byte
+// load: FINISHED even.)  Word 9 is unused.
+enum { PIPE_PAD_STEP = 9, PIPE_PAD_FINISHED = 10, PIPE_PAD_FLIP = 11, PIPE_PAD_MISGUESS = 12, PIPE_PAD_WORDS = 16 };
 template <class T>
 struct PipeArgs {
     PeerNb<T> nb[9];

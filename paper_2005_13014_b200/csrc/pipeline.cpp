@@ -248,9 +248,9 @@ oec_status oec_hdiff_pipeline_run(oec_hdiff_pipeline *p, int32_t nsteps, void *s
 oec_status oec_hdiff_pipeline_steps(const oec_hdiff_pipeline *p, int64_t *steps) {
     if (!p || !steps) return set_error(OEC_ERR_ARG, "oec_hdiff_pipeline_steps: NULL argument");
     unsigned long long v = 0;
-    cudaError_t e = cudaMemcpy(&v, p->pad + PIPE_PAD_STEP, sizeof v, cudaMemcpyDeviceToHost);
+    cudaError_t e = cudaMemcpy(&v, p->pad + PIPE_PAD_FINISHED, sizeof v, cudaMemcpyDeviceToHost);
     if (e != cudaSuccess) return set_error(OEC_ERR_CUDA, "oec_hdiff_pipeline_steps: %s", cudaGetErrorString(e));
-    *steps = (int64_t)v;
+    *steps = (int64_t)(v >> 20);  // one step = 2^20 (hdiff.cu PIPE_STEP_SHIFT)
     return OEC_OK;
 }
 

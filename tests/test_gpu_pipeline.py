@@ -141,6 +141,46 @@ def test_pipeline_single_rank_many_steps():
     check(ranks, ref, T)
 
 
+def _pad_word(pipe, w):
+    """Word w of a pipeline's device signal pad (diagnostic counters, csrc/oec_internal.h)."""
+    import torch
+
+    from paper_2005_13014_b200 import oec
+
+    ptr, nbytes = pipe.signal_pad()
+    arr = oec._CudaArray(ptr, (nbytes // 8,), (8,), pipe, "<u8")
+    return int(torch.as_tensor(arr, device="cuda:0")[w].item())
+
+
+def _set_pad_word(pipe, w, v):
+    import torch
+
+    from paper_2005_13014_b200 import oec
+
+    ptr, nbytes = pipe.signal_pad()
+    arr = oec._CudaArray(ptr, (nbytes // 8,), (8,), pipe, "<u8")
+    torch.as_tensor(arr, device="cuda:0")[w] = v
+
+
+@pytest.mark.parametrize("gdom,T", [((64, 4, 1), 5), ((150, 37, 3), 4), ((256, 256, 8), 3)])
+def test_pipeline_wrong_step_guess_recovers(gdom, T):
+    """The first tiles of a step are requested from the x_t of a GUESSED step before the step
+    counter is read; a wrong guess drains those loads and requests them again from the right
+    buffer.  Pad word 11 (a test hook) inverts every guess: the results must be unaffected and
+    pad word 12 must count the re-requests."""
+    import torch
+
+    host = synth.make_inputs("hdiff", gdom, seed=21)
+    ref = oracle_steps(host, gdom, T)
+    ranks = build_ranks(host, gdom, 1, 1, np.float64)
+    _set_pad_word(ranks[0]["pipe"], 11, 1)
+    torch.cuda.synchronize()
+    ranks[0]["pipe"].run(T)
+    torch.cuda.synchronize()
+    check(ranks, ref, T)
+    assert _pad_word(ranks[0]["pipe"], 12) >= T
+
+
 def test_pipeline_errors():
     from paper_2005_13014_b200 import oec
 
