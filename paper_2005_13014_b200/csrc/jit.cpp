@@ -1442,7 +1442,7 @@ static oec_status run_variant(const Program &P, const oec_field *const *in, oec_
                 continue;
             }
             const int box[3] = {L.w[q], L.h[q], L.dpt[q]};
-            if (!(P.in_kinv[q] ? make_tmap2d(in[q], box, &tm[q]) : make_tmap(in[q], box, &tm[q])))
+            if (!(P.in_kinv[q] ? make_tmap2d(in[q], box, &tm[q]) : make_tmap(in[q], box, &tm[q], JIT_PROMO)))
                 return set_error(OEC_ERR_LAYOUT, "%s: input %s cannot be described to TMA (OEC_VARIANT_TILED needs "
                                  "16-byte aligned rows and strides, e.g. oec_field_create)", P.name.c_str(),
                                  P.in_names[q].c_str());
@@ -1576,7 +1576,7 @@ static bool tiled_possible(const Program &P, const oec_field *const *in, const i
         ++n;
         TMap tm;
         const int box[3] = {L.w[q], L.h[q], L.dpt[q]};
-        if (!(P.in_kinv[q] ? make_tmap2d(in[q], box, &tm) : make_tmap(in[q], box, &tm))) return false;
+        if (!(P.in_kinv[q] ? make_tmap2d(in[q], box, &tm) : make_tmap(in[q], box, &tm, JIT_PROMO))) return false;
     }
     return n > 0 && L.smem <= 227 * 1024;
 }

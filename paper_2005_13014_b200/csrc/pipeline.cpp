@@ -166,7 +166,8 @@ oec_status oec_hdiff_pipeline_create(const int64_t global_domain[3], int32_t px,
     if (dt == OEC_F32) hdiff_pipe_boxes<float>(p->d, bin, bcf, &p->tile_w, &p->tile_jb);
     else hdiff_pipe_boxes<double>(p->d, bin, bcf, &p->tile_w, &p->tile_jb);
     const int64_t esz = dt == OEC_F32 ? 4 : 8;
-    bool ok = make_tmap(x0, bin, &p->m[0]) && make_tmap(x1, bin, &p->m[1]) && make_tmap(coeff, bcf, &p->mcf);
+    bool ok = make_tmap(x0, bin, &p->m[0], HD_PROMO) && make_tmap(x1, bin, &p->m[1], HD_PROMO) &&
+              make_tmap(coeff, bcf, &p->mcf, HD_PROMO);
     for (const oec_field *f : {x0, x1}) {  // i = 0 of every row on a 16-byte boundary (vector stores)
         const uintptr_t i0 = (uintptr_t)f->data + (uintptr_t)(-f->lb[0] * esz);
         ok = ok && i0 % 16 == 0 && (f->stride[1] * esz) % 16 == 0 && (f->stride[2] * esz) % 16 == 0;

@@ -426,7 +426,7 @@ static oec_status run_device(int p, const oec_field *const *in, oec_field *const
         TMap tin, tcf;
         int bin[3], bcf[3];
         hdiff_tma_boxes<T>(d, bin, bcf);
-        const bool tma = variant == OEC_VARIANT_AUTO && make_tmap(in[0], bin, &tin) && make_tmap(in[1], bcf, &tcf);
+        const bool tma = variant == OEC_VARIANT_AUTO && make_tmap(in[0], bin, &tin, HD_PROMO) && make_tmap(in[1], bcf, &tcf, HD_PROMO);
         e = launch_hdiff<T>(v_in[0], v_in[1], v_out[0], d, variant, aligned16, tma ? &tin : nullptr, tma ? &tcf : nullptr,
                          s, &launches);
         break;
