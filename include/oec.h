@@ -350,7 +350,8 @@ oec_status oec_halo_exchange_local_periodic(const int64_t global_domain[3], int3
  * (column) become neighbours -- with px == 1 (py == 1) the rank exchanges with ITSELF, which is
  * how the NCCL transport is exercised on one GPU.  Receive boxes then lie outside [0, global
  * domain) in the receiver's frame (oec_decomp_plan) and equal the sender's box modulo the
- * period.  NCCL pairs a rank's messages to one peer in issue order: oec_halo_exchange issues
+ * period.  Periodic i with non-periodic j: the i-exchange also carries the global outer j-halo
+ * rows (caller data), so the corners beyond a periodic i edge hold the wrapped columns' values.  NCCL pairs a rank's messages to one peer in issue order: oec_halo_exchange issues
  * them by (peer, tag, field) on both sides.  Errors: OEC_ERR_ARG (NULL d). */
 oec_status oec_decomp_set_periodic(oec_decomp *d, int32_t periodic_i, int32_t periodic_j);
 

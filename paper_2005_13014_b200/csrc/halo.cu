@@ -153,13 +153,18 @@ std::vector<oec_halo_msg> make_plan(const int64_t g[3], int px, int py, int rank
     const int right = ri < px - 1 ? rank + 1 : per_i ? rank - px + 1 : -1;
     const int down = rj > 0 ? rank - px : per_j ? rank + (py - 1) * px : -1;
     const int up = rj < py - 1 ? rank + px : per_j ? rank - (py - 1) * px : -1;
+    // phase-0 rows: the interior j-range; with a periodic i and a NON-periodic j, also the global
+    // outer j-halo rows at the domain's j edges (caller data on every rank): the corner cells
+    // beyond a periodic i edge are the wrapped columns' caller data, held by the i-neighbour
+    const int64_t j0 = lo[1] - (per_i && !per_j && rj == 0 ? wlo[1] : 0);
+    const int64_t j1 = hi[1] + (per_i && !per_j && rj == py - 1 ? whi[1] : 0);
     if (left >= 0) {  // left neighbour: it needs our first whi[0] columns, we need its last wlo[0]
-        add(left, 1, 0, 0, lo[0], lo[0] + whi[0], lo[1], hi[1]);
-        add(left, 0, 0, 1, lo[0] - wlo[0], lo[0], lo[1], hi[1]);
+        add(left, 1, 0, 0, lo[0], lo[0] + whi[0], j0, j1);
+        add(left, 0, 0, 1, lo[0] - wlo[0], lo[0], j0, j1);
     }
     if (right >= 0) {
-        add(right, 1, 0, 1, hi[0] - wlo[0], hi[0], lo[1], hi[1]);
-        add(right, 0, 0, 0, hi[0], hi[0] + whi[0], lo[1], hi[1]);
+        add(right, 1, 0, 1, hi[0] - wlo[0], hi[0], j0, j1);
+        add(right, 0, 0, 0, hi[0], hi[0] + whi[0], j0, j1);
     }
     // phase 1: j-neighbours, i-range including the i-halo (corners)
     const int64_t i0 = lo[0] - wlo[0], i1 = hi[0] + whi[0];

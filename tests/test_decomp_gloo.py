@@ -152,6 +152,7 @@ def test_decomposed_equals_global(program, gdom, px, py, w):
     ("hdiff", (12, 10, 2), 2, 1, ((2, 2, 0), (2, 2, 0)), (True, True)),  # the same peer on both sides in i
     ("hdiff", (13, 11, 2), 2, 2, ((2, 2, 0), (2, 2, 0)), (True, True)),
     ("vadv", (14, 5, 6), 2, 1, ((0, 0, 0), (1, 0, 0)), (True, False)),
+    ("hdiff", (13, 9, 2), 3, 1, ((2, 2, 0), (2, 2, 0)), (True, False)),  # corners beyond the periodic i edge
 ])
 def test_periodic_decomposed_equals_wrapped_global(program, gdom, px, py, w, per):
     # periodic domain (oec_decomp_set_periodic): the result equals the oracle on the global field
