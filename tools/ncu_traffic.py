@@ -19,14 +19,20 @@ round-2 captures showed ~1.7-2 MB per evict that is not the kernel's output).
 """
 import csv
 import json
+
+import numpy as np
 import os
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
+BASE, REP = 6, 3  # baseline evicts; measured launches per program (median taken)
 CONFIGS = {"c2": ((128, 128, 80), ("hdiff", "vadv")),
            "c3": ((128, 128, 80), ("hdiff", "vadv", "uvbke", "p_grad_c", "nh_p_grad", "fvtp2d_qi", "fvtp2d_qj",
+                                   "fvtp2d_flux", "fastwaves")),
+           "c4": ((1024, 1024, 80), ("hdiff", "vadv")),
+           "c5": ((512, 512, 80), ("hdiff", "vadv", "uvbke", "p_grad_c", "nh_p_grad", "fvtp2d_qi", "fvtp2d_qj",
                                    "fvtp2d_flux", "fastwaves"))}
 
 
@@ -42,7 +48,7 @@ def run(cfg):
     # baseline: three evicts back to back -- the DRAM writes of an evict that follows a clean L2
     # (its own partial sums and whatever else the driver writes back) are subtracted from the
     # write-back charged to the evict after each kernel
-    for _ in range(3):
+    for _ in range(BASE):
         evict.sum()
     torch.cuda.synchronize()
     for p in progs:
@@ -54,8 +60,9 @@ def run(cfg):
         oec.oec_apply_program(p, ins, outs, sc, (0, 0, 0), dom)  # warm-up (JIT tuning for the suite)
         torch.cuda.synchronize()
         evict.sum()
-        oec.oec_apply_program(p, ins, outs, sc, (0, 0, 0), dom)
-        evict.sum()
+        for _ in range(REP):  # evict, then REP x (kernel, evict): each kernel starts on a clean L2
+            oec.oec_apply_program(p, ins, outs, sc, (0, 0, 0), dom)
+            evict.sum()
         torch.cuda.synchronize()
         print(f"ran {p}", flush=True)
 
@@ -85,20 +92,25 @@ def parse(path, cfg):
     while q < len(seq) and "reduce" not in seq[q][0].lower():
         q += 1
     base = 0.0
-    if all("reduce" in seq[q + t][0].lower() for t in range(3)):  # the baseline evicts (run())
-        base = 0.5 * (to_bytes(seq[q + 1][1]["dram__bytes_write.sum"]) + to_bytes(seq[q + 2][1]["dram__bytes_write.sum"]))
-        q += 3
+    if all("reduce" in seq[q + t][0].lower() for t in range(BASE)):  # the baseline evicts (run())
+        base = float(np.median([to_bytes(seq[q + t][1]["dram__bytes_write.sum"]) for t in range(1, BASE)]))
+        q += BASE
     for p in progs:
-        # skip the warm-up launches until the reduce that precedes the timed kernel
+        # skip the warm-up launches until the reduce that precedes the measured kernels
         while q < len(seq) and "reduce" not in seq[q][0].lower():
             q += 1
-        name, m = seq[q + 1]
-        after = seq[q + 2][1]
-        rd_b, wr_b = to_bytes(m["dram__bytes_read.sum"]), to_bytes(m["dram__bytes_write.sum"])
-        wb = to_bytes(after["dram__bytes_write.sum"])
+        reps = []
+        for _ in range(REP):
+            name, m = seq[q + 1]
+            after = seq[q + 2][1]
+            rd_b, wr_b = to_bytes(m["dram__bytes_read.sum"]), to_bytes(m["dram__bytes_write.sum"])
+            wb = to_bytes(after["dram__bytes_write.sum"])
+            reps.append((rd_b + wr_b + max(0.0, wb - base), rd_b, wr_b, wb, m))
+            q += 2
+        q += 1
+        traffic, rd_b, wr_b, wb, m = sorted(reps, key=lambda x: x[0])[REP // 2]  # the median launch
         out[p] = {"kernel": name[:80], "read": rd_b, "write_in_kernel": wr_b, "write_back_after": wb,
-                  "evict_baseline_write": base, "traffic": rd_b + wr_b + max(0.0, wb - base), "duration_us": m["gpu__time_duration.sum"][0] / (1e3 if m["gpu__time_duration.sum"][1] in ("ns", "nsecond") else 1)}
-        q += 3
+                  "evict_baseline_write": base, "traffic": traffic, "traffic_all": [x[0] for x in reps], "duration_us": m["gpu__time_duration.sum"][0] / (1e3 if m["gpu__time_duration.sum"][1] in ("ns", "nsecond") else 1)}
     dst = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     allv = {}
     if os.path.exists(dst):

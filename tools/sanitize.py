@@ -7,7 +7,8 @@ The cases cover every kernel that synchronises through mbarriers / TMA / TMEM / 
   hdiff_tma         hdiff, TMA-ring kernel (small-size configuration)
   hdiff_tma_large   hdiff, the >= 8M-point tile configuration
   hdiff_pipe        the fused-exchange pipeline, 2x1 ranks on one device, 3 steps
-  vadv_sp           vadv, single wave (one column block per CTA, 4-chunk ring)
+  hdiff_pipe_flip   the same with every step-parity guess inverted (the re-request path)
+  vadv_sp           vadv, single wave (one column block per CTA, 5-chunk ring)
   vadv_sp_pers      vadv, persistent grid: CTAs walk several column blocks (ring + TMEM reuse)
   vadv_sp_multi     vadv, more CTAs than 12 per SM: 2D grid, 5-chunk ring
   jit_tiled         a suite program through the JIT's TMA-tiled variant
@@ -55,8 +56,8 @@ def jit_tiled(program, domain):
     print(f"{program} {domain} stencil-language JIT, tiled variant: bit-identical")
 
 
-def case_hdiff_pipe():
-    from test_gpu_pipeline import build_ranks, check, oracle_steps
+def case_hdiff_pipe(flip=False):
+    from test_gpu_pipeline import _set_pad_word, build_ranks, check, oracle_steps
 
     gdom = (96, 64, 6)
     host = synth.make_inputs("hdiff", gdom, seed=5)
@@ -64,18 +65,23 @@ def case_hdiff_pipe():
     T = 3
     import torch
 
+    if flip:
+        for R in ranks:
+            _set_pad_word(R["pipe"], 11, 1)
+        torch.cuda.synchronize()
     for _ in range(T):
         for R in ranks:
             R["pipe"].run(1)
     torch.cuda.synchronize()
     check(ranks, oracle_steps(host, gdom, T), T)
-    print("hdiff_pipe 2x1 ranks, 3 steps: bit-identical")
+    print(f"hdiff_pipe 2x1 ranks, 3 steps{' (guesses inverted)' if flip else ''}: bit-identical")
 
 
 CASES = {
     "hdiff_tma": lambda: parity("hdiff", (128, 64, 6)),
     "hdiff_tma_large": lambda: parity("hdiff", (1024, 1024, 8)),
     "hdiff_pipe": case_hdiff_pipe,
+    "hdiff_pipe_flip": lambda: case_hdiff_pipe(True),
     "vadv_sp": lambda: parity("vadv", (128, 16, 80)),
     "vadv_sp_pers": lambda: parity("vadv", (256, 160, 20)),  # 320 blocks on <= 148 CTAs
     "vadv_sp_multi": lambda: parity("vadv", (128, 1800, 8)),  # 1800 blocks > 12 x 148: 2D grid, 5 chunks
