@@ -85,3 +85,20 @@ def test_branch_free_rcp32_is_ieee_exhaustive():
 
     bad, used = oec.oec_selftest_rcp32()
     assert used > 3_000_000_000 and bad == 0, (bad, used)
+
+
+@pytest.mark.parametrize("case", range(27))
+def test_f32_randomized_shapes(case):
+    """Seeded random configurations in binary32 (as test_gpu_parity.test_randomized_shapes)."""
+    rng = np.random.default_rng(2000 + case)
+    program = synth.ALL_PROGRAMS[case % len(synth.ALL_PROGRAMS)]
+    ni, nj = int(rng.integers(1, 97)), int(rng.integers(1, 97))
+    nk = int(rng.integers(2 if program == "vadv" else 1, 41))
+    domain = (ni, nj, nk)
+    lo = tuple(int(rng.integers(0, max(1, n // 3))) for n in domain)
+    hi = tuple(int(rng.integers(l + 1, n + 1)) for l, n in zip(lo, domain))
+    if program == "vadv" and hi[2] - lo[2] < 2:
+        lo, hi = (lo[0], lo[1], 0), (hi[0], hi[1], nk)
+    order = [None, (0, 1, 2)][int(rng.integers(0, 2))]
+    out_halo = (int(rng.integers(0, 3)), int(rng.integers(0, 3)), 0)
+    _check(program, domain, seed=case, order=order, dom_lb=lo, dom_ub=hi, out_halo=out_halo)

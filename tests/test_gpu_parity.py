@@ -340,3 +340,22 @@ def test_every_program_c5_size_sampled(program):
     boxes = [((0, 0, 0), (40, 24, nk)), ((ni - 40, nj - 24, 0), (ni, nj, nk)), ((230, 250, kk[0]), (300, 270, kk[1])),
              ((0, nj - 10, 0), (ni, nj, nk if program == "vadv" else 3))]
     _check_sampled(program, (ni, nj, nk), boxes, seed=16)
+
+
+@pytest.mark.parametrize("case", range(48))
+def test_randomized_shapes(case):
+    """Seeded random configurations (program, domain, sub-domain box, layout, output halo): every
+    kernel-selection path (tile remainders in i and j, persistent / 2D vadv grids, short columns,
+    odd offsets) against the oracle, bit for bit, with nothing written outside the box."""
+    rng = np.random.default_rng(1000 + case)
+    program = synth.ALL_PROGRAMS[case % len(synth.ALL_PROGRAMS)]
+    ni, nj = int(rng.integers(1, 97)), int(rng.integers(1, 97))
+    nk = int(rng.integers(2 if program == "vadv" else 1, 41))
+    domain = (ni, nj, nk)
+    lo = tuple(int(rng.integers(0, max(1, n // 3))) for n in domain)
+    hi = tuple(int(rng.integers(l + 1, n + 1)) for l, n in zip(lo, domain))
+    if program == "vadv" and hi[2] - lo[2] < 2:  # the Thomas solve needs K >= 2
+        lo, hi = (lo[0], lo[1], 0), (hi[0], hi[1], nk)
+    order = ORDERS[int(rng.integers(0, 2))]
+    out_halo = (int(rng.integers(0, 3)), int(rng.integers(0, 3)), 0)
+    _check(program, domain, seed=case, order=order, dom_lb=lo, dom_ub=hi, out_halo=out_halo)
