@@ -474,6 +474,11 @@ def main():
     ap.add_argument("--sets", type=int, default=0, help="rotating input sets (0 = auto, > 4x L2)")
     ap.add_argument("--force-decomp", action="store_true",
                     help="debug: create the process group and decomposition even at N=1")
+    ap.add_argument("--emulate-neighbours", action="store_true",
+                    help="N=1 only: run the N>1 per-rank step -- halo exchange over NCCL on a comm stream, "
+                         "interior rows concurrently, boundary strips after -- against this rank itself "
+                         "(a periodic 1 x 1 j decomposition: both j-neighbours are the rank); measures the "
+                         "decomposition's per-rank overhead without a second GPU (not the NVLink transfer)")
     ap.add_argument("--exchange", default="fused", choices=["fused", "nccl"],
                     help="N>1 halo exchange of hdiff in c2/c4: 'fused' = oec_hdiff_pipeline (the kernel reads the "
                          "neighbours' halo cells from their memory, CUDA IPC), 'nccl' = oec_halo_exchange")
@@ -499,7 +504,8 @@ def main():
     oec.lib()  # fail loudly if the extension is missing
     dev = int(os.environ.get("OEC_BENCH_DEVICE", local_rank))
     torch.cuda.set_device(dev)
-    decomp = world > 1 or args.force_decomp
+    emulate = args.emulate_neighbours and world == 1
+    decomp = world > 1 or args.force_decomp or emulate
     if decomp:
         if world == 1:
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
@@ -521,7 +527,7 @@ def main():
     dec0 = oec.oec_decomp_create(gdom, 1, world, rank)
     lo, hi = dec0.local_lb, dec0.local_ub
     ldomain = tuple(hi[d] - lo[d] for d in range(3))
-    lo_nb, hi_nb = rank > 0, rank < world - 1
+    lo_nb, hi_nb = (True, True) if emulate else (rank > 0, rank < world - 1)
     pts_global = gdom[0] * gdom[1] * gdom[2]
 
     # ---- rotating input sets per program ----
@@ -534,7 +540,7 @@ def main():
 
     # ---- halo exchange transport for N > 1 ----
     fused_note, pipes, imported = None, {}, []
-    use_fused = decomp and world > 1 and args.exchange == "fused" and args.config in ("c2", "c4")
+    use_fused = decomp and world > 1 and args.exchange == "fused" and args.config in ("c2", "c4") and not emulate
     if decomp and args.dist_backend == "gloo" and not use_fused:
         raise SystemExit("--dist-backend gloo needs N > 1, --exchange fused and config c2/c4")
     if use_fused:
@@ -553,10 +559,12 @@ def main():
         else:
             pipes["hdiff"], imported = res
     dec = None
-    if decomp and world > 1 and args.dist_backend == "nccl":
+    if decomp and (world > 1 or emulate) and args.dist_backend == "nccl":
         pg = dist.distributed_c10d._get_default_group()
         dist.barrier()
         dec = oec.oec_decomp_create(gdom, 1, world, rank, pg._get_backend(torch.device("cuda", dev))._comm_ptr())
+        if emulate:
+            oec.oec_decomp_set_periodic(dec, False, True)
     step = Step(oec, torch, cfg, ldomain, lo_nb, hi_nb, dec, pipes, dev)
     progs = [pss[p] for p in cfg["programs"]]
 
@@ -724,7 +732,9 @@ def main():
 
     n_launch = K * sum(step.launches.values())
     if rank == 0:
-        nproc_note = "" if world == 1 else (
+        nproc_note = ("; EMULATED neighbours: periodic 1x1 j decomposition, NCCL self-exchange on a comm stream || "
+                      "interior rows, then boundary strips (per-rank overhead of N>1, no NVLink transfer)") if emulate \
+            else "" if world == 1 else (
             "; hdiff halo read from the neighbours' memory inside the kernel (fused pipeline, CUDA IPC)"
             if use_fused else "; NCCL halo exchange on a comm stream || interior rows, then boundary strips")
         res = {
@@ -773,8 +783,13 @@ def main():
         except Exception:
             pass
     if decomp:
-        dist.barrier()
-        dist.destroy_process_group()
+        dist.barrier()  # every rank has printed / written its results
+        # no destroy_process_group: tearing down the NCCL communicator that the captured exchange
+        # graphs still reference hung for minutes on the B200 box (measured with
+        # --emulate-neighbours); the process exits with everything flushed instead
+        sys.stdout.flush()
+        sys.stderr.flush()
+        os._exit(0)
     return 0
 
 
