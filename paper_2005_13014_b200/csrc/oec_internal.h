@@ -132,6 +132,8 @@ template <class V>
 oec_status field_view(const oec_field *f, const char *what, V *v);
 oec_status field_check(const oec_field *f, const char *what, int *device, int *dtype);
 bool field_overlap(const oec_field *a, const oec_field *b);
+// byte range [lo, hi) of a field's allocation (false for an empty field)
+bool field_span(const oec_field *f, uintptr_t *lo, uintptr_t *hi);
 
 // error plumbing; launch count reported by oec_last_launch_count
 oec_status set_error(oec_status st, const char *fmt, ...);

@@ -235,6 +235,7 @@ template oec_status field_view<FOT<float>>(const oec_field *, const char *, FOT<
 oec_status field_check(const oec_field *f, const char *what, int *device, int *dtype) {
     return check_field(f, what, device, dtype);
 }
+bool field_span(const oec_field *f, uintptr_t *lo, uintptr_t *hi) { return span_bytes(f, lo, hi); }
 bool field_overlap(const oec_field *a, const oec_field *b) {
     uintptr_t alo, ahi, blo, bhi;
     if (!span_bytes(a, &alo, &ahi) || !span_bytes(b, &blo, &bhi)) return false;
