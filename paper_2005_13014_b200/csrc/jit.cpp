@@ -704,7 +704,7 @@ static TileLayout tile_layout(const Program &P, const Spec &S, int esz) {
     L.stage_bytes = at;
     // 2..4 stages, at most ~110 KB per CTA so two CTAs share an SM
     L.stages = at > 0 ? std::max(2, std::min(4, (cta_kb * 1024) / std::max(at, 1))) : 1;
-    L.smem = L.stages * at + 8 * L.stages + 16;
+    L.smem = L.stages * at + 2 * 8 * L.stages + 16;  // ring + full / empty barriers
     return L;
 }
 
@@ -1181,6 +1181,14 @@ __device__ __forceinline__ void pf3(const TM *m, int c0, int c1, int c2) {
                  "r"(c1), "r"(c2) : "memory"); }
 )";
 
+// experiment (round 2, profiles/r02/jit_tiled_producer_ab.md): a producer warp refilling stages
+// behind per-stage empty barriers instead of a CTA-wide barrier per item -- 1.5-3% faster for
+// nh_p_grad / fvtp2d_qj with the 110 KB ring, up to 30% slower with the 56 KB one: off
+#ifndef JIT_TILED_PRODUCER
+#define JIT_TILED_PRODUCER 0
+#endif
+static constexpr int TILED_THREADS = JIT_TILED_PRODUCER ? 288 : 256;  // 8 compute warps (+ a producer warp)
+
 static std::string gen_tiled(const Program &P, const Spec &S) {
     const int esz = S.dtype == OEC_F32 ? 4 : 8;
     const TileLayout L = tile_layout(P, S, esz);
@@ -1201,9 +1209,10 @@ static std::string gen_tiled(const Program &P, const Spec &S) {
     for (size_t q = 0; q < P.out_names.size(); ++q) prm << sep << "T *__restrict__ g" << q;
     for (size_t q = 0; q < P.sc_names.size(); ++q) prm << sep << "const T s" << q;
     const int NI = L.ntile[0] * L.ntile[1] * L.ntile[2];
-    o << "extern \"C\" __global__ void __launch_bounds__(256) oec_jit_tiled(" << prm.str() << ") {\n"
+    o << "extern \"C\" __global__ void __launch_bounds__(" << TILED_THREADS << ") oec_jit_tiled(" << prm.str() << ") {\n"
       << "    extern __shared__ __align__(128) unsigned char smem[];\n"
       << "    unsigned long long *full = reinterpret_cast<unsigned long long *>(smem + " << L.stages * L.stage_bytes << ");\n"
+      << "    unsigned long long *empty = full + " << L.stages << ";\n"
       << "    const int tid = threadIdx.x, tx = tid % " << L.ti << ", ty = tid / " << L.ti << ";\n"
       << "    const int NITEMS = " << NI << ";\n";
     // TMA issue of one item's boxes into stage `st`, emitted inline where it is used (a lambda
@@ -1236,7 +1245,7 @@ static std::string gen_tiled(const Program &P, const Spec &S) {
     // the previous kernel's drain; every thread waits for it before touching its data
     o << "    asm volatile(\"griddepcontrol.launch_dependents;\" ::: \"memory\");\n"
       << "    if (tid == 0) {\n"
-      << "        for (int s = 0; s < " << L.stages << "; ++s) mb_init(&full[s], 1);\n"
+      << "        for (int s = 0; s < " << L.stages << "; ++s) { mb_init(&full[s], 1); mb_init(&empty[s], 8); }\n"
       << "        asm volatile(\"fence.mbarrier_init.release.cluster;\" ::: \"memory\");\n"
       << "        for (int s = 0; s < " << L.stages << "; ++s)\n"
       << "            if (blockIdx.x + s * gridDim.x < NITEMS)\n"
@@ -1248,8 +1257,24 @@ static std::string gen_tiled(const Program &P, const Spec &S) {
       << "            if (blockIdx.x + s * gridDim.x < NITEMS)\n"
       << issue("            ", "blockIdx.x + s * gridDim.x", "s")
       << "    }\n"
-      << "    __syncthreads();\n"
-      << "    for (int n = 0;; ++n) {\n"
+      << "    __syncthreads();\n";
+#if JIT_TILED_PRODUCER
+    // a producer warp refills a stage once the 8 compute warps have arrived on its empty barrier:
+    // no CTA-wide barrier per item (round 1's __syncthreads was the top stall, ncu)
+    o << "    if (tid >= 256) {\n"
+      << "        if (tid == 256)\n"
+      << "            for (int n = " << L.stages << ";; ++n) {\n"
+      << "                const int nxt = blockIdx.x + n * gridDim.x;\n"
+      << "                if (nxt >= NITEMS) break;\n"
+      << "                const int sp = n % " << L.stages << ";\n"
+      << "                mb_wait(&empty[sp], ((n / " << L.stages << ") - 1) & 1);\n"
+      << "                asm volatile(\"fence.proxy.async.shared::cta;\" ::: \"memory\");\n"
+      << issue("                ", "nxt", "sp")
+      << "            }\n"
+      << "        return;\n"
+      << "    }\n";
+#endif
+    o << "    for (int n = 0;; ++n) {\n"
       << "        const int item = blockIdx.x + n * gridDim.x;\n"
       << "        if (item >= NITEMS) break;\n"
       << "        const int st = n % " << L.stages << ";\n"
@@ -1290,17 +1315,21 @@ static std::string gen_tiled(const Program &P, const Spec &S) {
                 << "] = " << vals[u][q] << ";\n";
         E.o << E.ind << "}\n";
     }
-    o << E.o.str()
-      << "        }\n"
-      << "        __syncthreads();  // every thread is done with stage st\n"
+    o << E.o.str() << "        }\n";
+#if JIT_TILED_PRODUCER
+    o << "        __syncwarp();\n"
+      << "        if ((tid & 31) == 0) asm volatile(\"mbarrier.arrive.shared::cta.b64 _, [%0];\" ::\"r\"(su32(&empty[st])) : \"memory\");\n";
+#else
+    o << "        __syncthreads();  // every thread is done with stage st\n"
       << "        if (tid == 0) {\n"
       << "            const int nxt = item + " << L.stages << " * gridDim.x;\n"
       << "            if (nxt < NITEMS) {\n"
       << "                asm volatile(\"fence.proxy.async.shared::cta;\" ::: \"memory\");\n"
       << issue("                ", "nxt", "st")
       << "            }\n"
-      << "        }\n"
-      << "    }\n"
+      << "        }\n";
+#endif
+    o << "    }\n"
       << "}\n";
     return o.str();
 }
@@ -1476,7 +1505,7 @@ static oec_status run_variant(const Program &P, const oec_field *const *in, oec_
             CUlaunchConfig cfg = {};
             cfg.gridDimX = grid;
             cfg.gridDimY = cfg.gridDimZ = 1;
-            cfg.blockDimX = 256;
+            cfg.blockDimX = TILED_THREADS;
             cfg.blockDimY = cfg.blockDimZ = 1;
             cfg.sharedMemBytes = (unsigned)L.smem;
             cfg.hStream = (CUstream)s;
@@ -1487,7 +1516,7 @@ static oec_status run_variant(const Program &P, const oec_field *const *in, oec_
             cfg.numAttrs = 1;
             r = g_drv.launch_ex(&cfg, C->fns[0], args.data(), nullptr);
         } else {
-            r = g_drv.launch(C->fns[0], grid, 1, 1, 256, 1, 1, (unsigned)L.smem, (CUstream)s, args.data(), nullptr);
+            r = g_drv.launch(C->fns[0], grid, 1, 1, TILED_THREADS, 1, 1, (unsigned)L.smem, (CUstream)s, args.data(), nullptr);
         }
         if (r != CUDA_SUCCESS) return set_error(OEC_ERR_CUDA, "%s: cuLaunchKernel (tiled) failed (%d)", P.name.c_str(), (int)r);
         ++launches;
