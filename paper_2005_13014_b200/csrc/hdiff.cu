@@ -82,7 +82,7 @@
 #define HFL_NW 12
 #endif
 #ifndef HD_PF
-#define HD_PF 2  // tiles per warp prefetched into L2 before griddepcontrol.wait
+#define HD_PF 1  // tiles per warp prefetched into L2 before griddepcontrol.wait (round 2: 1 beats 2 by 1.5% at 128^2, profiles/r02/hdiff_cfg_r02.md)
 #endif
 #ifndef HD_LARGE_POINTS
 #define HD_LARGE_POINTS (8ll << 20)  // measured: the small tiles win up to 256^2 x 80 (0.79 -> 0.83)
