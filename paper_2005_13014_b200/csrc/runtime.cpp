@@ -357,6 +357,19 @@ static cudaError_t d2h_box(const oec_field *host, const oec_field *dev, const in
                                    (hi[2] - lo[2]) * ni * nj * es, cudaMemcpyDeviceToHost, s);
         }
     }
+    // whole dense i rows, k outermost (a j-slab of a numpy-style [k][j][i] field): the box's rows
+    // of one level are contiguous -- one 2D copy over the levels (round 1 issued one 2D copy per
+    // level: 80 API calls per field and slab, which made the slab pipeline slower than one slab)
+    {
+        const int64_t ni = host->ub[0] - host->lb[0];
+        if (!is_k_invariant(host) && host->stride[1] == ni && host->stride[2] >= ni * (host->ub[1] - host->lb[1]) &&
+            dev->stride[1] == ni && dev->stride[2] == host->stride[2] && lo[0] == host->lb[0] && hi[0] == host->ub[0]) {
+            const int es = esize(host->dtype);
+            const int64_t off = (lo[1] - host->lb[1]) * ni + (lo[2] - host->lb[2]) * host->stride[2];
+            return cudaMemcpy2DAsync((char *)host->data + off * es, host->stride[2] * es, (const char *)dev->data + off * es,
+                                     dev->stride[2] * es, (hi[1] - lo[1]) * ni * es, hi[2] - lo[2], cudaMemcpyDeviceToHost, s);
+        }
+    }
     // outer loop over the dimension with the larger stride, 2D copies over the other two
     int outer = (host->stride[2] >= host->stride[1]) ? 2 : 1;
     int mid = 3 - outer;
@@ -631,9 +644,10 @@ static oec_status apply(const ProgDesc &P, const oec_field *const *in, int n_in,
     static int max_slabs = -1;
     if (max_slabs < 0) {
         const char *ev = getenv("OEC_STAGE_SLABS");
-        // default 1: measured on the B200 box, overlapping H2D and D2H slabs made the 128x128x80
-        // step slower (1 slab 2.43 ms, 2: 2.84, 4: 3.89, 8: 5.29 ms; profiles/e2e_probe_r01d.txt)
-        max_slabs = ev ? std::max(1, std::min(STAGE_SLABS, atoi(ev))) : 1;
+        // default 2 (round 2): with the slab's D2H as one 2D copy (round 1 issued one per level,
+        // which made 2 slabs slower than 1), the 128x128x80 step is 1.85 ms with 1 slab, 1.79 with
+        // 2 or 3, 1.80 with 4 (profiles/r02/e2e_slabs_r02.txt)
+        max_slabs = ev ? std::max(1, std::min(STAGE_SLABS, atoi(ev))) : 2;
     }
     const int ns = (int)std::max<int64_t>(1, std::min<int64_t>(std::min<int64_t>(max_slabs, nj / 4),
                                                                   (int64_t)(total >> 22)));  // >= ~4 MB per slab
