@@ -51,7 +51,7 @@ def rank_fields(oec, torch, host, spec, gdom, lo, hi, per, order=None):
         own = (ii >= lo[0]) & (ii < hi[0]) & (jj >= lo[1]) & (jj < hi[1])
         out_i = (ii < 0) | (ii >= gdom[0])
         out_j = (jj < 0) | (jj >= gdom[1])
-        caller = (out_i & ~per[0]) | (out_j & ~per[1])
+        caller = (out_i & (not per[0])) | (out_j & (not per[1]))
         src[:, ~(own | caller)] = np.nan
         v[:, gl[1] - lo[1] - f.lb[1]:gh[1] - lo[1] - f.lb[1], gl[0] - lo[0] - f.lb[0]:gh[0] - lo[0] - f.lb[0]] = \
             torch.from_numpy(src)
