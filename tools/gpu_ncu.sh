@@ -22,4 +22,4 @@ for p in ${FULL_PROGRAMS:-hdiff vadv}; do
       > gpurun_out/${TAG}_full_${p}.log 2>&1
   echo "full $p rc=$?" >> gpurun_out/${TAG}_full_${p}.log
 done
-tail -2 gpurun_out/${TAG}_*.log
+for f in gpurun_out/${TAG}_*.log; do tail -n 2 $f; done
