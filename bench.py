@@ -815,6 +815,8 @@ def e2e_measure(oec, torch, progs, ldomain, steps, world, pts_global):
         d2h += len(outs) * ni * nj * nk * 8
         calls.append((ps, ins, outs))
 
+    # (measured: the programs' calls on their own streams from a thread pool -- concurrent host
+    # staging per stream -- took 1.96 ms per step against 1.79 on one stream; kept sequential)
     def step():
         for ps, ins, outs in calls:
             if ps.program == "hdiff":

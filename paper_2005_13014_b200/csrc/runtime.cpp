@@ -11,6 +11,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <map>
 #include <memory>
 #include <mutex>
 #include <vector>
@@ -283,47 +284,39 @@ struct Staging {
     cudaStream_t h2d = nullptr, d2h = nullptr;  // copy streams of the pipelined host path
     cudaEvent_t ev[2 * STAGE_SLABS] = {};
 };
-static Staging g_stage;
+// One staging set per (device, caller stream): host-path calls on different streams run
+// concurrently -- e.g. one program's H2D while another's D2H, PCIe being full duplex -- and calls
+// on one stream are serialised by its set's mutex.  A set lives for the life of the process
+// (its buffers only grow), so a caller should reuse a few streams, not create one per call.
+static std::mutex g_stages_mu;
+static std::map<std::pair<int, cudaStream_t>, std::unique_ptr<Staging>> g_stages;
 
-// the staging buffers, copy streams and events belong to one device: when the calling thread's
-// current device changes, release them (on their device) and start over on the new one
-static void stage_bind_device() {
-    int cur = 0;
-    cudaGetDevice(&cur);
-    if (g_stage.device == cur) return;
-    if (g_stage.device >= 0) {
-        int keep = cur;
-        cudaSetDevice(g_stage.device);
-        for (void *b : g_stage.bufs)
-            if (b) cudaFree(b);
-        if (g_stage.h2d) {
-            cudaStreamDestroy(g_stage.h2d);
-            cudaStreamDestroy(g_stage.d2h);
-            for (auto &e : g_stage.ev) cudaEventDestroy(e);
-        }
-        cudaSetDevice(keep);
+static Staging &stage_for(cudaStream_t s) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lock(g_stages_mu);
+    auto &p = g_stages[std::make_pair(dev, s)];
+    if (!p) {
+        p.reset(new Staging);
+        p->device = dev;
     }
-    g_stage.bufs.clear();
-    g_stage.sizes.clear();
-    g_stage.h2d = g_stage.d2h = nullptr;
-    for (auto &e : g_stage.ev) e = nullptr;
-    g_stage.device = cur;
+    return *p;
 }
 
-static oec_status stage_buffer(size_t idx, size_t bytes, void **p) {
-    if (g_stage.bufs.size() <= idx) {
-        g_stage.bufs.resize(idx + 1, nullptr);
-        g_stage.sizes.resize(idx + 1, 0);
+static oec_status stage_buffer(Staging &S, size_t idx, size_t bytes, void **p) {
+    if (S.bufs.size() <= idx) {
+        S.bufs.resize(idx + 1, nullptr);
+        S.sizes.resize(idx + 1, 0);
     }
-    if (g_stage.sizes[idx] < bytes) {
-        if (g_stage.bufs[idx]) cudaFree(g_stage.bufs[idx]);
-        g_stage.bufs[idx] = nullptr;
-        g_stage.sizes[idx] = 0;
-        cudaError_t e = cudaMalloc(&g_stage.bufs[idx], bytes);
+    if (S.sizes[idx] < bytes) {
+        if (S.bufs[idx]) cudaFree(S.bufs[idx]);
+        S.bufs[idx] = nullptr;
+        S.sizes[idx] = 0;
+        cudaError_t e = cudaMalloc(&S.bufs[idx], bytes);
         if (e != cudaSuccess) return set_error(OEC_ERR_CUDA, "staging cudaMalloc(%zu): %s", bytes, cudaGetErrorString(e));
-        g_stage.sizes[idx] = bytes;
+        S.sizes[idx] = bytes;
     }
-    *p = g_stage.bufs[idx];
+    *p = S.bufs[idx];
     return OEC_OK;
 }
 
@@ -608,8 +601,8 @@ static oec_status apply(const ProgDesc &P, const oec_field *const *in, int n_in,
     // slab s+1 (copy stream), the kernel on slab s (the caller's stream) and the D2H copy of slab
     // s-1 (a third stream) overlap -- PCIe is full duplex.  Each input row is copied once, in the
     // first slab that needs it; the call returns when the outputs are back in host memory.
-    std::lock_guard<std::mutex> lock(g_stage.mu);
-    stage_bind_device();  // the device twins live on the caller's current device
+    Staging &S = stage_for(s);  // the device twins live on the caller's current device
+    std::lock_guard<std::mutex> lock(S.mu);
     std::vector<oec_field> din(P_n_in), dout(P_n_out);
     std::vector<const oec_field *> pin(P_n_in);
     std::vector<oec_field *> pout(P_n_out);
@@ -618,9 +611,9 @@ static oec_status apply(const ProgDesc &P, const oec_field *const *in, int n_in,
         uintptr_t b0, b1;
         span_bytes(in[q], &b0, &b1);
         void *dptr;
-        if ((st = stage_buffer(slot++, b1 - b0, &dptr))) return st;
+        if ((st = stage_buffer(S, slot++, b1 - b0, &dptr))) return st;
         din[q] = *in[q];
-        din[q].device = g_stage.device;
+        din[q].device = S.device;
         din[q].data = (char *)dptr + ((uintptr_t)in[q]->data - b0);
         pin[q] = &din[q];
         total += b1 - b0;
@@ -629,16 +622,16 @@ static oec_status apply(const ProgDesc &P, const oec_field *const *in, int n_in,
         uintptr_t b0, b1;
         span_bytes(out[q], &b0, &b1);
         void *dptr;
-        if ((st = stage_buffer(slot++, b1 - b0, &dptr))) return st;
+        if ((st = stage_buffer(S, slot++, b1 - b0, &dptr))) return st;
         dout[q] = *out[q];
-        dout[q].device = g_stage.device;
+        dout[q].device = S.device;
         dout[q].data = (char *)dptr + ((uintptr_t)out[q]->data - b0);
         pout[q] = &dout[q];
     }
-    if (!g_stage.h2d) {
-        cudaStreamCreateWithFlags(&g_stage.h2d, cudaStreamNonBlocking);
-        cudaStreamCreateWithFlags(&g_stage.d2h, cudaStreamNonBlocking);
-        for (int e = 0; e < 2 * STAGE_SLABS; ++e) cudaEventCreateWithFlags(&g_stage.ev[e], cudaEventDisableTiming);
+    if (!S.h2d) {
+        cudaStreamCreateWithFlags(&S.h2d, cudaStreamNonBlocking);
+        cudaStreamCreateWithFlags(&S.d2h, cudaStreamNonBlocking);
+        for (int e = 0; e < 2 * STAGE_SLABS; ++e) cudaEventCreateWithFlags(&S.ev[e], cudaEventDisableTiming);
     }
     const int64_t nj = hi[1] - lo[1];
     static int max_slabs = -1;
@@ -659,7 +652,7 @@ static oec_status apply(const ProgDesc &P, const oec_field *const *in, int n_in,
             uintptr_t b0, b1;
             span_bytes(in[q], &b0, &b1);
             cudaError_t e0 = cudaMemcpyAsync((char *)din[q].data - ((uintptr_t)in[q]->data - b0), (const void *)b0,
-                                             b1 - b0, cudaMemcpyHostToDevice, g_stage.h2d);
+                                             b1 - b0, cudaMemcpyHostToDevice, S.h2d);
             if (e0 != cudaSuccess) return set_error(OEC_ERR_CUDA, "H2D copy of %s: %s", P.in_names[q].c_str(),
                                                     cudaGetErrorString(e0));
             next_row[q] = in[q]->ub[1];
@@ -671,20 +664,20 @@ static oec_status apply(const ProgDesc &P, const oec_field *const *in, int n_in,
         int64_t slo[3] = {lo[0], lo[1] + nj * sl / ns, lo[2]}, shi[3] = {hi[0], lo[1] + nj * (sl + 1) / ns, hi[2]};
         for (int q = 0; q < P_n_in && e == cudaSuccess; ++q) {  // rows this slab needs, not copied yet
             int64_t need = sl == ns - 1 ? in[q]->ub[1] : std::min<int64_t>(in[q]->ub[1], shi[1] + P.in_hi[q][1]);
-            if (need > next_row[q]) e = h2d_rows(&din[q], in[q], next_row[q], need, g_stage.h2d);
+            if (need > next_row[q]) e = h2d_rows(&din[q], in[q], next_row[q], need, S.h2d);
             next_row[q] = std::max(next_row[q], need);
         }
         if (e != cudaSuccess) break;
-        cudaEventRecord(g_stage.ev[2 * sl], g_stage.h2d);
-        cudaStreamWaitEvent(s, g_stage.ev[2 * sl], 0);
+        cudaEventRecord(S.ev[2 * sl], S.h2d);
+        cudaStreamWaitEvent(s, S.ev[2 * sl], 0);
         if ((st = P.run(dtype, pin.data(), pout.data(), sc.data(), slo, shi, variant, s))) return st;
         launches += g_launches;
-        cudaEventRecord(g_stage.ev[2 * sl + 1], s);
-        cudaStreamWaitEvent(g_stage.d2h, g_stage.ev[2 * sl + 1], 0);
-        for (int q = 0; q < P_n_out && e == cudaSuccess; ++q) e = d2h_box(out[q], &dout[q], slo, shi, g_stage.d2h);
+        cudaEventRecord(S.ev[2 * sl + 1], s);
+        cudaStreamWaitEvent(S.d2h, S.ev[2 * sl + 1], 0);
+        for (int q = 0; q < P_n_out && e == cudaSuccess; ++q) e = d2h_box(out[q], &dout[q], slo, shi, S.d2h);
     }
     if (e != cudaSuccess) return set_error(OEC_ERR_CUDA, "%s: host staging copy: %s", pname, cudaGetErrorString(e));
-    e = cudaStreamSynchronize(g_stage.d2h);
+    e = cudaStreamSynchronize(S.d2h);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
     if (e != cudaSuccess) return set_error(OEC_ERR_CUDA, "%s: %s", pname, cudaGetErrorString(e));
     g_launches = launches;

@@ -159,6 +159,42 @@ def test_host_buffers_end_to_end(program):
         assert np.all(a[m] == SENTINEL)
 
 
+def test_host_buffers_concurrent_streams():
+    # host-path calls from several threads on their own streams (staging per device and stream):
+    # every program's result equals the oracle, repeatedly, with the calls overlapping
+    from concurrent.futures import ThreadPoolExecutor
+
+    import torch
+
+    from paper_2005_13014_b200 import oec
+
+    domain = (96, 40, 12)
+    progs = ["hdiff", "vadv", "fvtp2d_qj", "uvbke"]
+    jobs = []
+    for q, program in enumerate(progs):
+        host = synth.make_inputs(program, domain, seed=30 + q)
+        spec = synth.PROGRAMS[program]
+        ins = [oec.oec_field_wrap(host[s.name].data, host[s.name].lb, host[s.name].ub, k_invariant=s.k_invariant)
+               for s in spec.inputs]
+        outs_np = [np.full((domain[2], domain[1], domain[0]), SENTINEL) for _ in spec.outputs]
+        outs = [oec.oec_field_wrap(a, (0, 0, 0), domain) for a in outs_np]
+        jobs.append((program, ins, outs, outs_np, run_oracle(program, host, domain), torch.cuda.Stream()))
+
+    def call(job):
+        program, ins, outs, _, _, st = job
+        oec.oec_apply_program(program, ins, outs, None, (0, 0, 0), domain, stream=st)
+
+    with ThreadPoolExecutor(max_workers=len(jobs)) as pool:
+        for _ in range(3):
+            for job in jobs:
+                for a in job[3]:
+                    a.fill(SENTINEL)
+            list(pool.map(call, jobs))
+            for program, _, _, outs_np, ref, _ in jobs:
+                for name, a in zip(synth.PROGRAMS[program].outputs, outs_np):
+                    assert np.array_equal(a, ref[name]), (program, name)
+
+
 def test_alias_rejected_on_device():
     from paper_2005_13014_b200 import oec
 
