@@ -79,10 +79,23 @@
 #define HFL_S 2
 #endif
 #ifndef HFL_NW
-#define HFL_NW 12
+#define HFL_NW 8  // round 2: two 8-warp CTAs per SM, f32 1024^2 210.6 -> 197.4 us (f64 keeps 12: 381.6 vs 393.1)
 #endif
 #ifndef HD_PF
 #define HD_PF 1  // tiles per warp prefetched into L2 before griddepcontrol.wait (round 2: 1 beats 2 by 1.5% at 128^2, profiles/r02/hdiff_cfg_r02.md)
+#endif
+// tiny domains (<= HD_TINY_POINTS, e.g. 128x128x80): the same tiles in CTAs of HD_TNW warps, two
+// per SM (16 warps instead of 12; an SM starts a CTA of the next launch as soon as one of its two
+// finishes): 128^2 x 80 f64 6.76 -> 6.57 us, f32 4.65 -> 4.38; 256x256x60 keeps 12-warp CTAs
+// (16.2 vs 16.7 us; profiles/r02/hdiff_nw_r02.md)
+#ifndef HD_TNW
+#define HD_TNW 8
+#endif
+#ifndef HF_TNW
+#define HF_TNW 8
+#endif
+#ifndef HD_TINY_POINTS
+#define HD_TINY_POINTS (2ll << 20)
 #endif
 #ifndef HD_LARGE_POINTS
 #define HD_LARGE_POINTS (8ll << 20)  // measured: the small tiles win up to 256^2 x 80 (0.79 -> 0.83)
@@ -932,19 +945,22 @@ cudaError_t launch_roll(const FVT<T> &in, const FVT<T> &coeff, const FOT<T> &out
 static bool hdiff_large(const Dom &d) {
     return (long long)(d.hi[0] - d.lo[0]) * (d.hi[1] - d.lo[1]) * (d.hi[2] - d.lo[2]) >= HD_LARGE_POINTS;
 }
+static bool hdiff_tiny(const Dom &d) {
+    return (long long)(d.hi[0] - d.lo[0]) * (d.hi[1] - d.lo[1]) * (d.hi[2] - d.lo[2]) <= HD_TINY_POINTS;
+}
 
 // tile configuration per element type: f32 tiles have the same bytes per row as f64 (V doubled)
 template <class T>
 struct HdCfg;
 template <>
 struct HdCfg<double> {
-    static constexpr int V = HD_V, JB = HD_JB, S = HD_S, NW = HD_NW;
+    static constexpr int V = HD_V, JB = HD_JB, S = HD_S, NW = HD_NW, TNW = HD_TNW;
     static constexpr int LV = HDL_V, LJB = HDL_JB, LS = HDL_S, LNW = HDL_NW;
     static constexpr int RV = 2;  // rolling kernel vector width when 16-byte aligned
 };
 template <>
 struct HdCfg<float> {
-    static constexpr int V = HF_V, JB = HF_JB, S = HF_S, NW = HF_NW;
+    static constexpr int V = HF_V, JB = HF_JB, S = HF_S, NW = HF_NW, TNW = HF_TNW;
     static constexpr int LV = HFL_V, LJB = HFL_JB, LS = HFL_S, LNW = HFL_NW;
     static constexpr int RV = 4;
 };
@@ -979,6 +995,7 @@ cudaError_t launch_hdiff(const FVT<T> &in, const FVT<T> &coeff, const FOT<T> &ou
     }
     if (tin && tcf && aligned16) {
         if (hdiff_large(d)) return launch_tma<T, C::LV, C::LJB, C::LS, C::LNW>(*tin, *tcf, out, d, s, launches);
+        if (hdiff_tiny(d)) return launch_tma<T, C::V, C::JB, C::S, C::TNW>(*tin, *tcf, out, d, s, launches);
         return launch_tma<T, C::V, C::JB, C::S, C::NW>(*tin, *tcf, out, d, s, launches);
     }
     if (aligned16) return launch_roll<T, C::RV, 16, 4>(in, coeff, out, d, s, launches);
