@@ -38,7 +38,7 @@ def _oracle_chain(program, host, domain, chained):
     return r
 
 
-def _gpu_chain(program, host, domain, chained, graph):
+def _gpu_chain(program, host, domain, chained, graph, dtype=np.float64):
     import torch
 
     from paper_2005_13014_b200 import oec
@@ -58,7 +58,7 @@ def _gpu_chain(program, host, domain, chained, graph):
         s = torch.cuda.Stream()
         g = torch.cuda.CUDAGraph()
         # first call outside the capture (one-time setup: tensor maps, function attributes)
-        warm = [oec.field_from_host(host[chained]), oec.empty_like_domain(domain)]
+        warm = [oec.field_from_host(host[chained]), oec.empty_like_domain(domain, dtype=dtype)]
         ins = [warm[0] if s_.name == chained else fixed[s_.name] for s_ in spec.inputs]
         oec.oec_apply_program(program, ins, [warm[1]], sc, (0, 0, 0), domain, 0, None)
         torch.cuda.synchronize()
@@ -149,3 +149,14 @@ def test_hdiff_vadv_alternating(graph):
         f.data[:, 2:-2, 2:-2] = yo
         h["in"] = f
     assert compare(y.download(), yo)["n_bitdiff"] == 0, graph
+
+
+@pytest.mark.parametrize("program,chained", [("hdiff", "in"), ("vadv", "u_stage")])
+def test_f32_chain(program, chained):
+    # binary32: hdiff's 8-warp tier and vadv_sp<float> in graph-replayed chains
+    domain = (128, 128, 80)
+    host = synth.make_inputs(program, domain, seed=10, dtype=np.float32)
+    g = _gpu_chain(program, host, domain, chained, True, dtype=np.float32)
+    r = _oracle_chain(program, host, domain, chained)
+    c = compare(g, r)
+    assert c["n_bitdiff"] == 0 and not np.isnan(g).any(), (program, c)
