@@ -88,6 +88,9 @@
 // per SM (16 warps instead of 12; an SM starts a CTA of the next launch as soon as one of its two
 // finishes): 128^2 x 80 f64 6.76 -> 6.57 us, f32 4.65 -> 4.38; 256x256x60 keeps 12-warp CTAs
 // (16.2 vs 16.7 us; profiles/r02/hdiff_nw_r02.md)
+#ifndef HF_PF
+#define HF_PF HD_PF  // f32
+#endif
 #ifndef HD_TNW
 #define HD_TNW 8
 #endif
@@ -562,7 +565,7 @@ __global__ void __launch_bounds__(NW * 32, 1) hdiff_tma(const __grid_constant__ 
         for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
         fence_mbar_init();
 #pragma unroll
-        for (int s = 0; s < HD_PF; ++s)  // warm L2 with the first tiles during the previous kernel's drain
+        for (int s = 0; s < (sizeof(T) == 8 ? HD_PF : HF_PF); ++s)  // warm L2 with the first tiles during the previous kernel's drain
             if (gw + s * nwt < nitems) {
                 int ib, j0, k;
                 decode(gw + s * nwt, ib, j0, k);
